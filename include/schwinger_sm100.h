@@ -1,0 +1,153 @@
+/*
+ * schwinger_sm100.h — C-ABI of the B200 (sm_100a) engine for the HMC
+ * molecular-dynamics hot path of the 2D Schwinger model (arXiv:1512.03812
+ * reference package `schwinger`, /root/reference/pkg/src/schwinger).
+ *
+ * The reference has no FFI: its boundary is the in-process Python module API
+ * (SURVEY.md §8(b)).  Each entry point below replaces one reference function;
+ * the citation names it.  A ctypes binding (paper_1512_03812_b200/_lib.py)
+ * mirrors those Python signatures on top of this header; INTEGRATION.md shows
+ * the stub a maintainer of the reference would add.
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer unless named h_*; layouts are the
+ *    reference's (lattice.py:3-12):
+ *       links (q, p, forces)  double  [B][2][L][T]
+ *       link cache U          double  [B][2][L][T][2]   (re, im) = exp(i q)
+ *       spinors               double  [B][L][T][2][2]   complex128 (B, L, T, 2)
+ *    B = number of independent chains (batch), B >= 1.
+ *  - All work is stream-ordered on the context's stream (sch_set_stream);
+ *    calls return without synchronising unless stated.
+ *  - Return value: 0 = OK, 1 = bad argument, 2 = CUDA error,
+ *    3 = solver hit maxiter (details in the per-chain status array).
+ *    sch_last_error() gives the message.
+ *  - Arithmetic is IEEE FP64 throughout.  Real-arithmetic updates (drift,
+ *    kicks) are evaluated without FMA contraction in NumPy's order.
+ */
+#ifndef SCHWINGER_SM100_H
+#define SCHWINGER_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sch_ctx sch_ctx;
+
+/* ---- context --------------------------------------------------------- */
+int sch_ctx_create(int device, sch_ctx** out);
+int sch_ctx_destroy(sch_ctx* ctx);
+int sch_set_stream(sch_ctx* ctx, void* cuda_stream);
+const char* sch_last_error(const sch_ctx* ctx);
+/* Number of kernels this context has launched (for bench accounting). */
+unsigned long long sch_launch_count(const sch_ctx* ctx);
+/* Library build identifier, e.g. "sm_100a". */
+const char* sch_build_info(void);
+
+/* ---- L0: links, momenta (lattice.py) --------------------------------- */
+/* out = wrap(q + h*p), wrap = floored mod to [-pi,pi)
+ * replaces lattice.rotate_links (lattice.py:111-118) + wrap_angles (:28-30) */
+int sch_rotate_links(sch_ctx* ctx, const double* q, const double* p, double h,
+                     double* out, long long n);
+/* replaces lattice.wrap_angles (lattice.py:28-30) */
+int sch_wrap_angles(sch_ctx* ctx, const double* q, double* out, long long n);
+/* out = p - (a*f + c*g)   (g may be NULL => out = p - a*f)
+ * replaces the momentum kicks of integrators.py:161-246 / shift_momenta
+ * (lattice.py:121-125) */
+int sch_kick(sch_ctx* ctx, const double* p, const double* f, double a,
+             const double* g, double c, double* out, long long n);
+/* out[b] = 0.5 * sum p^2 over the chain's 2*L*T links
+ * replaces lattice.kinetic_energy (lattice.py:128-130) */
+int sch_kinetic_energy(sch_ctx* ctx, const double* p, double* out, int B, long long per_chain);
+
+/* ---- L1a: gauge sector (gauge.py) ------------------------------------ */
+/* theta(n) per site, [B][L][T]; replaces gauge.plaq_angles (gauge.py:21-24) */
+int sch_plaquette_angles(sch_ctx* ctx, const double* q, double* out, int B, int L, int T);
+/* beta * g (gauge.py:43-59) */
+int sch_gauge_force(sch_ctx* ctx, const double* q, double beta, double* out, int B, int L, int T);
+/* p_out = p - dt * (beta * g(q)); kick_gauge (integrators.py:161-164) fused */
+int sch_kick_gauge(sch_ctx* ctx, const double* q, const double* p, double beta, double dt,
+                   double* p_out, int B, int L, int T);
+/* M micro leapfrog steps of the gauge system fused: [kick dt/2, drift dt,
+ * kick dt/2] x m (integrators.py:253-259). q, p updated in place. */
+int sch_inner_leapfrog(sch_ctx* ctx, double* q, double* p, double beta, double span, int m,
+                       int B, int L, int T);
+/* per chain: beta*sum(1-cos theta) (gauge.py:37-40) and mean cos theta (gauge.py:32-34) */
+int sch_gauge_action(sch_ctx* ctx, const double* q, double beta, double* out, int B, int L, int T);
+int sch_avg_plaquette(sch_ctx* ctx, const double* q, double* out, int B, int L, int T);
+/* C_GG closed form (gauge.py:97-107) */
+int sch_fg_gauge_gauge(sch_ctx* ctx, const double* q, double beta, double* out, int B, int L, int T);
+/* 2 * sum w * Hess(S_G) (gauge.py:110-136) */
+int sch_gauge_hessian_dot(sch_ctx* ctx, const double* q, double beta, const double* w,
+                          double* out, int B, int L, int T);
+
+/* ---- L1b: Wilson fermions (fermion.py) ------------------------------- */
+/* U = exp(i q) (fermion.py:94); fermion_bc 0 = periodic (reference),
+ * 1 = antiperiodic in time (sign flip of U_t on t = T-1; BASELINE configs) */
+int sch_links_to_u(sch_ctx* ctx, const double* q, double* U, int B, int L, int T, int fermion_bc);
+/* out = D psi (dagger=0) or D^dag psi (dagger=1); U chain stride 0 when
+ * u_batched == 0.  replaces WilsonDirac.apply / apply_dag (fermion.py:119-127) */
+int sch_dslash(sch_ctx* ctx, const double* U, int u_batched, const double* psi, double* out,
+               int B, int L, int T, double m0, int dagger);
+/* out = D^dag D psi, fused (one pass, shared-memory halo tile)
+ * replaces WilsonDirac.normal (fermion.py:129-131) */
+int sch_ddagd(sch_ctx* ctx, const double* U, const double* psi, double* out,
+              int B, int L, int T, double m0);
+/* out[b] = sum conj(a) b over the chain (complex: out[2b], out[2b+1])
+ * replaces fermion.spinor_dot (fermion.py:54-56) */
+int sch_spinor_dot(sch_ctx* ctx, const double* a, const double* b, double* out, int B, long long V);
+
+/* CG on D^dag D x = b (fermion.py:171-217), exact stopping semantics:
+ * residual replacement every 50 iterations, true-residual re-check, alpha/beta
+ * guards.  stop_mode 0 = batch_global (reference batched semantics: every
+ * chain iterates until all pass), 1 = per_chain (each chain stops as an
+ * unbatched reference call would).  x0 may be NULL (zero start).
+ * Per-chain outputs (device): iters[B] (int32), relres[B] (true ||b-Ax||/||b||
+ * at convergence, or the best residual on failure), status[B] (0 ok,
+ * 1 maxiter).  h_iters_out (host, may be NULL) receives the max iteration
+ * count; requesting it synchronises the stream.
+ * Returns 3 (SCH_ERR_SOLVER) only when h_iters_out is non-NULL and a chain
+ * failed; otherwise failures are reported through status[] (no sync). */
+int sch_cg_normal(sch_ctx* ctx, const double* U, const double* b, double* x, const double* x0,
+                  int B, int L, int T, double m0, double tol, int maxiter, int stop_mode,
+                  int* iters, double* relres, int* status, int* h_iters_out);
+
+/* f(n,mu) = -Im[A - B] (fermion.py:330-336); when p != NULL the kick is
+ * fused: out = p - dt * (f [+ beta*g(q) when q != NULL])  (kick_fermion /
+ * kick_full, integrators.py:172-186) */
+int sch_fermion_force(sch_ctx* ctx, const double* U, const double* chi, const double* xi,
+                      double* out, int B, int L, int T);
+int sch_kick_fermion(sch_ctx* ctx, const double* U, const double* chi, const double* xi,
+                     const double* q, double beta, const double* p, double dt, double* p_out,
+                     int B, int L, int T);
+/* b1 = sum weight*w1, b2 = sum weight*w2 (fermion.py:362-383) */
+int sch_weighted_w_sums(sch_ctx* ctx, const double* U, const double* weight, const double* chi,
+                        const double* xi, double* b1, double* b2, int B, int L, int T);
+/* C = 2Im(A[z1,xi]-B[z1,xi]) + 2Im(A[chi,z2]-B[chi,z2]) - 2Re(A[chi,xi]+B[chi,xi])*weight
+ * (fermion.py:409-417) */
+int sch_fg_fermion_combine(sch_ctx* ctx, const double* U, const double* z1, const double* z2,
+                           const double* chi, const double* xi, const double* weight,
+                           double* out, int B, int L, int T);
+
+/* ---- L3: Metropolis on device (bench mode) -------------------------- */
+/* accept[b] = 1 if dH <= 0 or u < exp(-dH), 0 otherwise, -1 if dH is not
+ * finite (hmc.py:54-60) */
+int sch_metropolis(sch_ctx* ctx, const double* dh, const double* u, int* accept, int B);
+/* out[b] = accept[b] == 1 ? a[b] : b_[b] over per_chain doubles (hmc.py:95) */
+int sch_select_chains(sch_ctx* ctx, const int* accept, const double* a, const double* b_,
+                      double* out, int B, long long per_chain);
+
+/* ---- device RNG (bench mode; parity mode draws on the host with the
+ * reference's NumPy Philox generator) ---------------------------------- */
+/* scale * standard normals, Philox4x32-10 keyed by (seed, stream0 + chain),
+ * counter (ctr, element); out[b * per_chain + i] */
+int sch_rng_normal(sch_ctx* ctx, double* out, int B, long long per_chain, uint64_t seed,
+                   uint64_t stream0, uint64_t ctr, double scale);
+int sch_rng_uniform(sch_ctx* ctx, double* out, int B, long long per_chain, uint64_t seed,
+                    uint64_t stream0, uint64_t ctr);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCHWINGER_SM100_H */

@@ -1,0 +1,763 @@
+// Conjugate gradient on the Wilson normal operator D^dag D, with the exact
+// stopping semantics of the reference cg_normal (fermion.py:171-217):
+//
+//   normb = ||b||, target = tol*normb;  x = 0 | x0;  r = b - A x;  p = r
+//   for it = 1..maxiter:
+//     ap = A p;  alpha = <p,ap> > 0 ? rs/<p,ap> : 0;  x += alpha p
+//     r = (it % 50 == 0) ? b - A x : r - alpha ap;   rs' = ||r||^2
+//     if sqrt(rs') <= target:                        (true-residual re-check)
+//        tr = b - A x; if ||tr|| <= target: return;  r = tr; rs' = ||tr||^2
+//     beta = rs > 0 ? rs'/rs : 0;  p = r + beta p;  rs = rs'
+//
+// Two engines:
+//  * resident  : one CTA owns one chain for the whole solve (V <= 2048).  U,
+//                p and D p live in shared memory, x and r in registers; the
+//                solve is a single launch with no host round trips.  Used for
+//                per-chain stopping (the hmc_update semantics) — the 16^2 and
+//                32^2 ensembles of BASELINE configs 1-3.
+//  * streaming : HBM-resident vectors, one fused D^dag D tile pass + one
+//                fused update pass per iteration (352 B/site/iteration, SURVEY
+//                §8(d)), tiny per-chain control kernels, and a host loop that
+//                enqueues iterations in chunks and polls a device flag.  Used
+//                for batch_global stopping (measure_dh semantics) and lattices
+//                too large for one CTA (configs 4-5).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "runtime.hpp"
+#include "tile.cuh"
+#include "../../include/schwinger_sm100.h"
+
+namespace {
+
+constexpr int kReplace = 50;   // residual replacement period (fermion.py:199)
+
+// ============================================================ resident CG
+struct ResArgs {
+  const double2* __restrict__ U;   // [B][2][V]
+  const double2* __restrict__ b;   // [B][V][2]
+  const double2* __restrict__ x0;  // may be null
+  double2* __restrict__ x;         // out
+  double2* __restrict__ pscr;      // [B][V][2] scratch (rare path)
+  int* __restrict__ iters;
+  double* __restrict__ relres;
+  int* __restrict__ status;
+  int L, T;
+  double diag, tol;
+  int maxiter;
+};
+
+template <int NT, int SPT>
+__global__ void __launch_bounds__(NT) k_cg_resident(ResArgs a) {
+  extern __shared__ double2 sm[];
+  __shared__ double red[3][NT / 32];
+  const int L = a.L, T = a.T, V = L * T;
+  double2* sU0 = sm;
+  double2* sU1 = sm + V;
+  double2* sP0 = sm + 2 * V;
+  double2* sP1 = sm + 3 * V;
+  double2* sT0 = sm + 4 * V;
+  double2* sT1 = sm + 5 * V;
+  const int c = blockIdx.x;
+  const long long cb = (long long)c * V;
+  const int tid = threadIdx.x;
+
+  for (int i = tid; i < 2 * V; i += NT) sm[i] = a.U[2 * cb + i];
+
+  int site[SPT], nxp[SPT], nxm[SPT], ntp[SPT], ntm[SPT];
+  Spinor x[SPT], r[SPT];
+  double bb = 0.0;
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) {
+    int s = tid + k * NT;
+    site[k] = s < V ? s : -1;
+    if (s < V) {
+      int xx = s / T, tt = s - xx * T;
+      nxp[k] = (xx + 1 == L ? 0 : xx + 1) * T + tt;
+      nxm[k] = (xx == 0 ? L - 1 : xx - 1) * T + tt;
+      ntp[k] = xx * T + (tt + 1 == T ? 0 : tt + 1);
+      ntm[k] = xx * T + (tt == 0 ? T - 1 : tt - 1);
+      r[k] = ldg_spinor(a.b, cb + s);
+      bb += spinor_norm2(r[k]);
+    } else {
+      nxp[k] = nxm[k] = ntp[k] = ntm[k] = 0;
+      r[k].s0 = r[k].s1 = make_double2(0, 0);
+    }
+    x[k].s0 = x[k].s1 = make_double2(0, 0);
+  }
+  const double normb2 = block_sum<NT>(bb, red[0]);
+  const double normb = sqrt(normb2);
+  const double target = a.tol * normb;
+  if (normb == 0.0) {   // fermion.py:181-182 (per chain)
+#pragma unroll
+    for (int k = 0; k < SPT; ++k)
+      if (site[k] >= 0) st_spinor(a.x, cb + site[k], x[k]);
+    if (tid == 0) {
+      a.iters[c] = 0;
+      a.relres[c] = 0.0;
+      a.status[c] = 0;
+    }
+    return;
+  }
+
+  // D stage: sT = D sP on my sites; Ddag stage returns D^dag sT on my sites
+  auto stage_d = [&]() {
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      if (site[k] < 0) continue;
+      const int s = site[k];
+      Spinor cc{sP0[s], sP1[s]};
+      Spinor xp{sP0[nxp[k]], sP1[nxp[k]]}, xm{sP0[nxm[k]], sP1[nxm[k]]};
+      Spinor tp{sP0[ntp[k]], sP1[ntp[k]]}, tm{sP0[ntm[k]], sP1[ntm[k]]};
+      Spinor o = wilson_site<false>(cc, xp, xm, tp, tm, sU0[s], sU0[nxm[k]], sU1[s], sU1[ntm[k]],
+                                    a.diag);
+      sT0[s] = o.s0;
+      sT1[s] = o.s1;
+    }
+  };
+  auto stage_ddag = [&](int k) {
+    const int s = site[k];
+    Spinor cc{sT0[s], sT1[s]};
+    Spinor xp{sT0[nxp[k]], sT1[nxp[k]]}, xm{sT0[nxm[k]], sT1[nxm[k]]};
+    Spinor tp{sT0[ntp[k]], sT1[ntp[k]]}, tm{sT0[ntm[k]], sT1[ntm[k]]};
+    return wilson_site<true>(cc, xp, xm, tp, tm, sU0[s], sU0[nxm[k]], sU1[s], sU1[ntm[k]], a.diag);
+  };
+
+  double rs = normb2;   // r = b exactly: same sum as normb^2 (fermion.py:186,191)
+  if (a.x0) {
+#pragma unroll
+    for (int k = 0; k < SPT; ++k)
+      if (site[k] >= 0) {
+        x[k] = ldg_spinor(a.x0, cb + site[k]);
+        sP0[site[k]] = x[k].s0;
+        sP1[site[k]] = x[k].s1;
+      }
+    __syncthreads();
+    stage_d();
+    __syncthreads();
+    double rr = 0.0;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k)
+      if (site[k] >= 0) {
+        Spinor ax = stage_ddag(k);
+        r[k].s0 = csub(r[k].s0, ax.s0);
+        r[k].s1 = csub(r[k].s1, ax.s1);
+        rr += spinor_norm2(r[k]);
+      }
+    rs = block_sum<NT>(rr, red[1]);   // also orders the sP reads before the writes below
+  }
+#pragma unroll
+  for (int k = 0; k < SPT; ++k)
+    if (site[k] >= 0) {
+      sP0[site[k]] = r[k].s0;
+      sP1[site[k]] = r[k].s1;
+    }
+
+  double best = INFINITY;
+  for (int it = 1; it <= a.maxiter; ++it) {
+    __syncthreads();
+    stage_d();
+    __syncthreads();
+    Spinor ap[SPT];
+    double pap = 0.0;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      if (site[k] < 0) continue;
+      ap[k] = stage_ddag(k);
+      Spinor pk{sP0[site[k]], sP1[site[k]]};
+      pap += spinor_redot(pk, ap[k]);
+    }
+    const double den = block_sum<NT>(pap, red[0]);
+    const double alpha = den > 0.0 ? rs / den : 0.0;
+    const bool repl = (it % kReplace) == 0;
+    double rsn = 0.0;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      if (site[k] < 0) continue;
+      const int s = site[k];
+      double2 p0 = sP0[s], p1 = sP1[s];
+      x[k].s0 = make_double2(__fma_rn(alpha, p0.x, x[k].s0.x), __fma_rn(alpha, p0.y, x[k].s0.y));
+      x[k].s1 = make_double2(__fma_rn(alpha, p1.x, x[k].s1.x), __fma_rn(alpha, p1.y, x[k].s1.y));
+      if (!repl) {
+        r[k].s0 = make_double2(__fma_rn(-alpha, ap[k].s0.x, r[k].s0.x),
+                               __fma_rn(-alpha, ap[k].s0.y, r[k].s0.y));
+        r[k].s1 = make_double2(__fma_rn(-alpha, ap[k].s1.x, r[k].s1.x),
+                               __fma_rn(-alpha, ap[k].s1.y, r[k].s1.y));
+        rsn += spinor_norm2(r[k]);
+      }
+    }
+    double rs_new = 0.0;
+    bool check = true;
+    if (!repl) {
+      rs_new = block_sum<NT>(rsn, red[1]);
+      check = sqrt(rs_new) <= target;
+    }
+    bool from_scratch = false;
+    if (check) {
+      // true residual b - A x (residual replacement shares this path)
+#pragma unroll
+      for (int k = 0; k < SPT; ++k)
+        if (site[k] >= 0) {
+          a.pscr[2 * (cb + site[k])] = sP0[site[k]];
+          a.pscr[2 * (cb + site[k]) + 1] = sP1[site[k]];
+        }
+      __syncthreads();
+#pragma unroll
+      for (int k = 0; k < SPT; ++k)
+        if (site[k] >= 0) {
+          sP0[site[k]] = x[k].s0;
+          sP1[site[k]] = x[k].s1;
+        }
+      __syncthreads();
+      stage_d();
+      __syncthreads();
+      double tn2 = 0.0;
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        if (site[k] < 0) continue;
+        Spinor ax = stage_ddag(k);
+        Spinor bk = ldg_spinor(a.b, cb + site[k]);
+        ap[k].s0 = csub(bk.s0, ax.s0);
+        ap[k].s1 = csub(bk.s1, ax.s1);
+        tn2 += spinor_norm2(ap[k]);
+      }
+      tn2 = block_sum<NT>(tn2, red[2]);
+      const double tn = sqrt(tn2);
+      if (!repl || tn <= target) best = tn / normb;
+      if (tn <= target) {
+#pragma unroll
+        for (int k = 0; k < SPT; ++k)
+          if (site[k] >= 0) st_spinor(a.x, cb + site[k], x[k]);
+        if (tid == 0) {
+          a.iters[c] = it;
+          a.relres[c] = tn / normb;
+          a.status[c] = 0;
+        }
+        return;
+      }
+#pragma unroll
+      for (int k = 0; k < SPT; ++k)
+        if (site[k] >= 0) r[k] = ap[k];
+      rs_new = tn2;
+      from_scratch = true;
+    }
+    const double beta = rs > 0.0 ? rs_new / rs : 0.0;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      if (site[k] < 0) continue;
+      const int s = site[k];
+      double2 p0, p1;
+      if (from_scratch) {
+        p0 = a.pscr[2 * (cb + s)];
+        p1 = a.pscr[2 * (cb + s) + 1];
+      } else {
+        p0 = sP0[s];
+        p1 = sP1[s];
+      }
+      sP0[s] = make_double2(__fma_rn(beta, p0.x, r[k].s0.x), __fma_rn(beta, p0.y, r[k].s0.y));
+      sP1[s] = make_double2(__fma_rn(beta, p1.x, r[k].s1.x), __fma_rn(beta, p1.y, r[k].s1.y));
+    }
+    rs = rs_new;
+  }
+  // iteration cap (fermion.py:216-217)
+#pragma unroll
+  for (int k = 0; k < SPT; ++k)
+    if (site[k] >= 0) st_spinor(a.x, cb + site[k], x[k]);
+  if (tid == 0) {
+    a.iters[c] = a.maxiter;
+    a.relres[c] = fmin(best, sqrt(rs) / normb);
+    a.status[c] = 1;
+  }
+}
+
+template <int NT, int SPT>
+int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
+  const size_t smem = sizeof(double2) * 6 * (size_t)a.L * a.T;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_cg_resident<NT, SPT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  k_cg_resident<NT, SPT><<<B, NT, smem, ctx->stream>>>(a);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+// =========================================================== streaming CG
+struct StreamState {
+  // per chain
+  double *normb, *target, *rs, *rs_new, *alpha, *beta, *best;
+  int *active, *need_x, *pass;
+  // per chain outputs (caller-owned)
+  int* iters;
+  double* relres;
+  int* status;
+  // global
+  int* n_active;   // chains still iterating; 0 => done
+  int* n_active_init;
+  // partials [B][tpc]
+  double *part_pap, *part_rr, *part_rr2, *part_bb;
+  int B, tpc, global_mode;
+  double tol;
+  int maxiter;
+};
+
+// Elementwise pass over the same tiles as the stencil (so partials align).
+struct ElemArgs {
+  const double2* __restrict__ b;
+  const double2* __restrict__ x0;
+  double2* __restrict__ x;
+  double2* __restrict__ r;
+  double2* __restrict__ p;
+  const double2* __restrict__ ap;
+  int L, T, TX, TT, tiles_t, tpc;
+};
+
+__device__ __forceinline__ bool tile_site(const ElemArgs& e, int tile, int k, long long& s) {
+  const int tx = tile / e.tiles_t, tt = tile - (tile / e.tiles_t) * e.tiles_t;
+  const int li = k / e.TT, lj = k - (k / e.TT) * e.TT;
+  const int X = tx * e.TX + li, Tt = tt * e.TT + lj;
+  if (X >= e.L || Tt >= e.T) return false;
+  s = (long long)X * e.T + Tt;
+  return true;
+}
+
+// init: x = x0|0; r = b; p = b; partial ||b||^2
+__global__ void k_cg_init(ElemArgs e, StreamState st) {
+  __shared__ double slot[32];
+  const int c = blockIdx.x / e.tpc, tile = blockIdx.x - c * e.tpc;
+  const long long cb = (long long)c * e.L * e.T;
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < e.TX * e.TT; k += blockDim.x) {
+    long long s;
+    if (!tile_site(e, tile, k, s)) continue;
+    Spinor bv = ldg_spinor(e.b, cb + s);
+    acc += spinor_norm2(bv);
+    Spinor xv;
+    if (e.x0) xv = ldg_spinor(e.x0, cb + s);
+    else xv.s0 = xv.s1 = make_double2(0, 0);
+    st_spinor(e.x, cb + s, xv);
+    st_spinor(e.r, cb + s, bv);
+    st_spinor(e.p, cb + s, bv);
+  }
+  double s = block_sum_rt(acc, slot);
+  if (threadIdx.x == 0) st.part_bb[blockIdx.x] = s;
+}
+
+// p = r (after r = b - A x0)
+__global__ void k_copy_r_to_p(ElemArgs e) {
+  const int c = blockIdx.x / e.tpc, tile = blockIdx.x - c * e.tpc;
+  const long long cb = (long long)c * e.L * e.T;
+  for (int k = threadIdx.x; k < e.TX * e.TT; k += blockDim.x) {
+    long long s;
+    if (!tile_site(e, tile, k, s)) continue;
+    st_spinor(e.p, cb + s, ld_spinor(e.r, cb + s));
+  }
+}
+
+// update: p = r + beta p; x += alpha p; (non-replacement) r -= alpha ap, partial ||r||^2
+__global__ void k_cg_update(ElemArgs e, StreamState st, int repl) {
+  __shared__ double slot[32];
+  const int c = blockIdx.x / e.tpc, tile = blockIdx.x - c * e.tpc;
+  if (!st.active[c]) return;
+  const double al = st.alpha[c], be = st.beta[c];
+  const long long cb = (long long)c * e.L * e.T;
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < e.TX * e.TT; k += blockDim.x) {
+    long long s;
+    if (!tile_site(e, tile, k, s)) continue;
+    const long long o = 2 * (cb + s);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double2 rv = e.r[o + h], pv = e.p[o + h], xv = e.x[o + h];
+      pv = make_double2(__fma_rn(be, pv.x, rv.x), __fma_rn(be, pv.y, rv.y));
+      xv = make_double2(__fma_rn(al, pv.x, xv.x), __fma_rn(al, pv.y, xv.y));
+      e.p[o + h] = pv;
+      e.x[o + h] = xv;
+      if (!repl) {
+        double2 av = __ldg(e.ap + o + h);
+        rv = make_double2(__fma_rn(-al, av.x, rv.x), __fma_rn(-al, av.y, rv.y));
+        e.r[o + h] = rv;
+        acc += rv.x * rv.x + rv.y * rv.y;
+      }
+    }
+  }
+  if (!repl) {
+    double s = block_sum_rt(acc, slot);
+    if (threadIdx.x == 0) st.part_rr[blockIdx.x] = s;
+  }
+}
+
+__device__ __forceinline__ double sum_partials(const double* part, int tpc, int c, double* slot) {
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < tpc; k += blockDim.x) acc += part[(long long)c * tpc + k];
+  return block_sum_rt(acc, slot);
+}
+
+// init control: normb, target, rs, flags
+__global__ void k_ctrl_init(StreamState st, int have_x0) {
+  __shared__ double slot[2][32];
+  const int c = blockIdx.x;
+  double nb2 = sum_partials(st.part_bb, st.tpc, c, slot[0]);
+  double rr = have_x0 ? sum_partials(st.part_rr2, st.tpc, c, slot[1]) : nb2;
+  if (threadIdx.x == 0) {
+    double nb = sqrt(nb2);
+    st.normb[c] = nb;
+    st.target[c] = st.tol * nb;
+    st.rs[c] = rr;
+    st.beta[c] = 0.0;
+    st.alpha[c] = 0.0;
+    st.best[c] = INFINITY;
+    st.iters[c] = 0;
+    st.relres[c] = 0.0;
+    st.status[c] = 0;
+    st.need_x[c] = 0;
+    st.pass[c] = 0;
+    st.active[c] = st.global_mode ? 1 : (nb > 0.0 ? 1 : 0);
+  }
+}
+
+// one CTA: count active chains; global mode: all-zero rhs => done (fermion.py:181)
+__global__ void k_ctrl_init_global(StreamState st) {
+  __shared__ int cnt;
+  __shared__ int nz;
+  if (threadIdx.x == 0) {
+    cnt = 0;
+    nz = 0;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < st.B; c += blockDim.x) {
+    if (st.active[c]) atomicAdd(&cnt, 1);
+    if (st.normb[c] != 0.0) atomicAdd(&nz, 1);
+  }
+  __syncthreads();
+  if (st.global_mode && nz == 0) {
+    for (int c = threadIdx.x; c < st.B; c += blockDim.x) st.active[c] = 0;
+    if (threadIdx.x == 0) *st.n_active = *st.n_active_init = 0;
+    return;
+  }
+  if (threadIdx.x == 0) *st.n_active = *st.n_active_init = cnt;
+}
+
+// after the stencil pass: alpha = <p,Ap> > 0 ? rs/<p,Ap> : 0
+__global__ void k_ctrl_alpha(StreamState st) {
+  __shared__ double slot[32];
+  const int c = blockIdx.x;
+  if (!st.active[c]) return;
+  double den = sum_partials(st.part_pap, st.tpc, c, slot);
+  if (threadIdx.x == 0) st.alpha[c] = den > 0.0 ? st.rs[c] / den : 0.0;
+}
+
+// after the update: rs' and the convergence check
+__global__ void k_ctrl_check(StreamState st, int repl) {
+  __shared__ double slot[32];
+  const int c = blockIdx.x;
+  if (!st.active[c]) return;
+  if (repl) {
+    if (threadIdx.x == 0) {
+      st.pass[c] = 1;
+      st.need_x[c] = 1;
+    }
+    return;
+  }
+  double rsn = sum_partials(st.part_rr, st.tpc, c, slot);
+  if (threadIdx.x == 0) {
+    st.rs_new[c] = rsn;
+    int ok = sqrt(rsn) <= st.target[c];
+    st.pass[c] = ok;
+    st.need_x[c] = st.global_mode ? 0 : ok;
+  }
+}
+
+// global mode: the true-residual branch runs only when every chain passes
+__global__ void k_ctrl_check_global(StreamState st, int repl) {
+  __shared__ int fails;
+  if (threadIdx.x == 0) fails = 0;
+  __syncthreads();
+  if (!repl)
+    for (int c = threadIdx.x; c < st.B; c += blockDim.x)
+      if (st.active[c] && !st.pass[c]) atomicAdd(&fails, 1);
+  __syncthreads();
+  const int all = fails == 0;
+  for (int c = threadIdx.x; c < st.B; c += blockDim.x)
+    if (st.active[c]) st.need_x[c] = repl ? 1 : all;
+}
+
+// after the (optional) true-residual pass
+__global__ void k_ctrl_final(StreamState st, int it) {
+  __shared__ double slot[32];
+  const int c = blockIdx.x;
+  if (!st.active[c]) return;
+  const int nx = st.need_x[c];
+  double tn2 = nx ? sum_partials(st.part_rr2, st.tpc, c, slot) : 0.0;
+  if (threadIdx.x != 0) return;
+  double rs_new = nx ? tn2 : st.rs_new[c];
+  st.rs_new[c] = rs_new;
+  if (st.global_mode) return;   // decisions in k_ctrl_final_global
+  if (nx) {
+    const double tn = sqrt(tn2);
+    const int repl = (it % kReplace) == 0;
+    if (!repl || tn <= st.target[c]) st.best[c] = tn / st.normb[c];
+    if (tn <= st.target[c]) {
+      st.active[c] = 0;
+      st.iters[c] = it;
+      st.relres[c] = tn / st.normb[c];
+      atomicSub(st.n_active, 1);
+      return;
+    }
+  }
+  const double rs = st.rs[c];
+  st.beta[c] = rs > 0.0 ? rs_new / rs : 0.0;
+  st.rs[c] = rs_new;
+  st.need_x[c] = 0;
+  if (it >= st.maxiter) {
+    st.active[c] = 0;
+    st.iters[c] = it;
+    st.status[c] = 1;
+    st.relres[c] = fmin(st.best[c], sqrt(rs_new) / st.normb[c]);
+    atomicSub(st.n_active, 1);
+  }
+}
+
+__global__ void k_ctrl_final_global(StreamState st, int it) {
+  __shared__ int fails, any_x;
+  __shared__ double worst;
+  if (threadIdx.x == 0) {
+    fails = 0;
+    any_x = 0;
+    worst = 0.0;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < st.B; c += blockDim.x) {
+    if (!st.active[c]) continue;
+    if (st.need_x[c]) {
+      atomicOr(&any_x, 1);
+      if (!(sqrt(st.rs_new[c]) <= st.target[c])) atomicAdd(&fails, 1);
+    }
+  }
+  __syncthreads();
+  // worst relative true residual of this check (fermion.py:207), fixed order
+  if (any_x && threadIdx.x == 0) {
+    double w = 0.0;
+    for (int c = 0; c < st.B; ++c)
+      if (st.active[c] && st.normb[c] > 0) w = fmax(w, sqrt(st.rs_new[c]) / st.normb[c]);
+    worst = w;
+  }
+  __syncthreads();
+  const bool converged = any_x && fails == 0;
+  for (int c = threadIdx.x; c < st.B; c += blockDim.x) {
+    if (!st.active[c]) continue;
+    if (any_x && (!((it % kReplace) == 0) || converged)) st.best[c] = worst;
+    if (converged) {
+      st.active[c] = 0;
+      st.iters[c] = it;
+      st.relres[c] = st.normb[c] > 0 ? sqrt(st.rs_new[c]) / st.normb[c] : 0.0;
+      continue;
+    }
+    const double rs = st.rs[c], rsn = st.rs_new[c];
+    st.beta[c] = rs > 0.0 ? rsn / rs : 0.0;
+    st.rs[c] = rsn;
+    st.need_x[c] = 0;
+    if (it >= st.maxiter) {
+      st.active[c] = 0;
+      st.iters[c] = it;
+      st.status[c] = 1;
+      st.relres[c] = fmin(st.best[c], sqrt(rsn) / (st.normb[c] > 0 ? st.normb[c] : 1.0));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && (converged || it >= st.maxiter)) *st.n_active = 0;
+}
+
+// Chains whose rhs is exactly zero return x = 0 (fermion.py:181-182): per
+// chain in per-chain mode, and for the whole batch in global mode when every
+// rhs is zero.
+__global__ void k_zero_x_if_null(ElemArgs e, StreamState st) {
+  const int c = blockIdx.x / e.tpc, tile = blockIdx.x - c * e.tpc;
+  if (st.normb[c] != 0.0) return;
+  if (st.global_mode && *st.n_active_init != 0) return;
+  const long long cb = (long long)c * e.L * e.T;
+  for (int k = threadIdx.x; k < e.TX * e.TT; k += blockDim.x) {
+    long long s;
+    if (!tile_site(e, tile, k, s)) continue;
+    Spinor z;
+    z.s0 = z.s1 = make_double2(0, 0);
+    st_spinor(e.x, cb + s, z);
+  }
+}
+
+int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, const double2* x0,
+                 int B, int L, int T, double m0, double tol, int maxiter, int global_mode, int* iters,
+                 double* relres, int* status) {
+  const TileShape sh = pick_tile(L, T);
+  const int tpc = sh.tiles_x * sh.tiles_t;
+  const long long V = (long long)L * T;
+  const size_t nvec = (size_t)B * V * 2;   // double2 per vector
+  size_t bytes = 3 * nvec * sizeof(double2) + 7 * (size_t)B * sizeof(double) +
+                 3 * (size_t)B * sizeof(int) + 4 * (size_t)B * tpc * sizeof(double) + 64 * 256;
+  void* ws;
+  int rc = sch_workspace(ctx, bytes, &ws);
+  if (rc) return rc;
+  char* w = (char*)ws;
+  auto take = [&](size_t n) {
+    char* p = w;
+    w += (n + 255) & ~size_t(255);
+    return (void*)p;
+  };
+  double2* r = (double2*)take(nvec * sizeof(double2));
+  double2* p = (double2*)take(nvec * sizeof(double2));
+  double2* ap = (double2*)take(nvec * sizeof(double2));
+  StreamState st;
+  st.normb = (double*)take(B * 8);
+  st.target = (double*)take(B * 8);
+  st.rs = (double*)take(B * 8);
+  st.rs_new = (double*)take(B * 8);
+  st.alpha = (double*)take(B * 8);
+  st.beta = (double*)take(B * 8);
+  st.best = (double*)take(B * 8);
+  st.active = (int*)take(B * 4);
+  st.need_x = (int*)take(B * 4);
+  st.pass = (int*)take(B * 4);
+  st.n_active = (int*)take(4);
+  st.n_active_init = (int*)take(4);
+  st.part_pap = (double*)take((size_t)B * tpc * 8);
+  st.part_rr = (double*)take((size_t)B * tpc * 8);
+  st.part_rr2 = (double*)take((size_t)B * tpc * 8);
+  st.part_bb = (double*)take((size_t)B * tpc * 8);
+  if ((size_t)(w - (char*)ws) > ctx->ws_bytes)
+    return sch_fail(ctx, SCH_ERR_ARG, "cg workspace layout overflow");
+  st.iters = iters;
+  st.relres = relres;
+  st.status = status;
+  st.B = B;
+  st.tpc = tpc;
+  st.global_mode = global_mode;
+  st.tol = tol;
+  st.maxiter = maxiter;
+
+  ElemArgs e{b, x0, x, r, p, ap, L, T, sh.TX, sh.TT, sh.tiles_t, tpc};
+  TileArgs ta{};
+  ta.U = U;
+  ta.B = B;
+  ta.L = L;
+  ta.T = T;
+  ta.tiles_t = sh.tiles_t;
+  ta.tiles_per_chain = tpc;
+  ta.diag = 2.0 + m0;
+  const unsigned ngrid = (unsigned)B * tpc;
+  cudaStream_t s = ctx->stream;
+
+  k_cg_init<<<ngrid, 256, 0, s>>>(e, st);
+  SCH_LAUNCHED(ctx);
+  if (x0) {   // r = b - A x0 ; p = r
+    TileArgs tx = ta;
+    tx.in = x;
+    tx.bvec = b;
+    tx.out = r;
+    tx.flag = nullptr;
+    tx.partial = st.part_rr2;
+    launch_normal_tile<MODE_X>(sh, tx, s);
+    SCH_LAUNCHED(ctx);
+    k_copy_r_to_p<<<ngrid, 256, 0, s>>>(e);
+    SCH_LAUNCHED(ctx);
+  }
+  k_ctrl_init<<<B, 128, 0, s>>>(st, x0 != nullptr);
+  SCH_LAUNCHED(ctx);
+  k_ctrl_init_global<<<1, 1024, 0, s>>>(st);
+  SCH_LAUNCHED(ctx);
+
+  TileArgs tp = ta;   // stencil pass: p formed on the fly from r, p_old
+  tp.in = r;
+  tp.in2 = p;
+  tp.out = ap;
+  tp.flag = st.active;
+  tp.beta = st.beta;
+  tp.partial = st.part_pap;
+  TileArgs txx = ta;  // true residual / replacement pass
+  txx.in = x;
+  txx.bvec = b;
+  txx.out = r;
+  txx.flag = st.need_x;
+  txx.partial = st.part_rr2;
+
+  int it = 1;
+  int chunk = 4;
+  while (it <= maxiter) {
+    int n = std::min(chunk, maxiter - it + 1);
+    for (int j = 0; j < n; ++j, ++it) {
+      const int repl = (it % kReplace) == 0;
+      launch_normal_tile<MODE_P>(sh, tp, s);
+      SCH_LAUNCHED(ctx);
+      k_ctrl_alpha<<<B, 128, 0, s>>>(st);
+      SCH_LAUNCHED(ctx);
+      k_cg_update<<<ngrid, 256, 0, s>>>(e, st, repl);
+      SCH_LAUNCHED(ctx);
+      k_ctrl_check<<<B, 128, 0, s>>>(st, repl);
+      SCH_LAUNCHED(ctx);
+      if (global_mode) {
+        k_ctrl_check_global<<<1, 1024, 0, s>>>(st, repl);
+        SCH_LAUNCHED(ctx);
+      }
+      launch_normal_tile<MODE_X>(sh, txx, s);
+      SCH_LAUNCHED(ctx);
+      k_ctrl_final<<<B, 128, 0, s>>>(st, it);
+      SCH_LAUNCHED(ctx);
+      if (global_mode) {
+        k_ctrl_final_global<<<1, 1024, 0, s>>>(st, it);
+        SCH_LAUNCHED(ctx);
+      }
+    }
+    SCH_CUDA(ctx, cudaMemcpyAsync(ctx->h_flag, st.n_active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SCH_CUDA(ctx, cudaStreamSynchronize(s));
+    if (*ctx->h_flag == 0) break;
+    chunk = std::min(chunk * 2, 32);
+  }
+  k_zero_x_if_null<<<ngrid, 256, 0, s>>>(e, st);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+}  // namespace
+
+extern "C" int sch_cg_normal(sch_ctx* ctx, const double* U, const double* b, double* x,
+                             const double* x0, int B, int L, int T, double m0, double tol,
+                             int maxiter, int stop_mode, int* iters, double* relres, int* status,
+                             int* h_iters_out) {
+  SCH_CHECK_ARG(ctx, U && b && x && iters && relres && status, "cg_normal: null pointer");
+  SCH_CHECK_ARG(ctx, B >= 1 && L >= 2 && T >= 2 && maxiter >= 1, "cg_normal: bad geometry");
+  SCH_CHECK_ARG(ctx, stop_mode == 0 || stop_mode == 1, "cg_normal: stop_mode must be 0 or 1");
+  SCH_CHECK_ARG(ctx, x != b && x != x0, "cg_normal: x must not alias b or x0");
+  const long long V = (long long)L * T;
+  const bool per_chain = stop_mode == 1 || B == 1;
+  int rc = SCH_OK;
+  if (per_chain && V <= 2048) {
+    void* ws;
+    rc = sch_workspace(ctx, sizeof(double2) * 2 * (size_t)B * V, &ws);
+    if (rc) return rc;
+    ResArgs a{(const double2*)U, (const double2*)b, (const double2*)x0, (double2*)x, (double2*)ws,
+              iters, relres, status, L, T, 2.0 + m0, tol, maxiter};
+    if (V <= 128) rc = launch_resident<128, 1>(ctx, a, B);
+    else if (V <= 256) rc = launch_resident<128, 2>(ctx, a, B);
+    else if (V <= 512) rc = launch_resident<256, 2>(ctx, a, B);
+    else if (V <= 1024) rc = launch_resident<256, 4>(ctx, a, B);
+    else rc = launch_resident<512, 4>(ctx, a, B);
+  } else {
+    rc = cg_streaming(ctx, (const double2*)U, (const double2*)b, (double2*)x, (const double2*)x0, B,
+                      L, T, m0, tol, maxiter, per_chain ? 0 : 1, iters, relres, status);
+  }
+  if (rc) return rc;
+  if (h_iters_out) {
+    std::vector<int> hi(B), hs(B);
+    SCH_CUDA(ctx, cudaMemcpyAsync(hi.data(), iters, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    SCH_CUDA(ctx, cudaMemcpyAsync(hs.data(), status, sizeof(int) * B, cudaMemcpyDeviceToHost, ctx->stream));
+    SCH_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    *h_iters_out = *std::max_element(hi.begin(), hi.end());
+    for (int c = 0; c < B; ++c)
+      if (hs[c]) return sch_fail(ctx, SCH_ERR_SOLVER, "CG exceeded %d iterations (chain %d)", maxiter, c);
+  }
+  return SCH_OK;
+}

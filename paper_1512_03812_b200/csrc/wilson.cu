@@ -1,0 +1,369 @@
+// Wilson-fermion kernels: link cache, D / D^dag, fused D^dag D, spinor dots,
+// fermion force (+ fused kicks), weighted w-sums and the fermion
+// force-gradient contraction.  Reference: fermion.py.
+#include "common.cuh"
+#include "runtime.hpp"
+#include "tile.cuh"
+#include "../../include/schwinger_sm100.h"
+
+namespace {
+
+struct Geo {
+  int B, L, T;
+  long long V;
+};
+
+unsigned grid_for(long long n, int nt = 256) {
+  long long b = (n + nt - 1) / nt;
+  if (b > 148LL * 64) b = 148LL * 64;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+// U = exp(i q) = (cos q, sin q)  (fermion.py:94).  bc = 1 flips U_t on the
+// last time slice (fermions antiperiodic in time, BASELINE configs).
+__global__ void k_links_to_u(const double* __restrict__ q, double2* __restrict__ U, Geo g, int bc) {
+  long long n = (long long)g.B * 2 * g.V;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double s, c;
+    sincos(q[i], &s, &c);
+    if (bc) {
+      long long r = i % (2 * g.V);
+      if (r >= g.V && (r - g.V) % g.T == g.T - 1) {
+        s = -s;
+        c = -c;
+      }
+    }
+    U[i] = make_double2(c, s);
+  }
+}
+
+// One thread per site; neighbours through L1.  Used for the single-D
+// applications (chi = D xi, eta = D^dag phi, D^dag b for solve_dirac).
+template <bool DAG>
+__global__ void k_dslash(const double2* __restrict__ U, long long ustride,
+                         const double2* __restrict__ psi, double2* __restrict__ out, Geo g,
+                         double diag) {
+  long long n = (long long)g.B * g.V;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long b = i / g.V;
+    int s = (int)(i - b * g.V);
+    int x = s / g.T, t = s - x * g.T;
+    int xp = x + 1 == g.L ? 0 : x + 1, xm = x == 0 ? g.L - 1 : x - 1;
+    int tp = t + 1 == g.T ? 0 : t + 1, tm = t == 0 ? g.T - 1 : t - 1;
+    long long cb = b * g.V;
+    const double2* Uc = U + b * ustride;
+    Spinor c = ldg_spinor(psi, cb + s);
+    Spinor vxp = ldg_spinor(psi, cb + xp * g.T + t);
+    Spinor vxm = ldg_spinor(psi, cb + xm * g.T + t);
+    Spinor vtp = ldg_spinor(psi, cb + x * g.T + tp);
+    Spinor vtm = ldg_spinor(psi, cb + x * g.T + tm);
+    double2 u0 = __ldg(Uc + s), u1 = __ldg(Uc + g.V + s);
+    double2 u0m = __ldg(Uc + xm * g.T + t), u1m = __ldg(Uc + g.V + x * g.T + tm);
+    st_spinor(out, cb + s, wilson_site<DAG>(c, vxp, vxm, vtp, vtm, u0, u0m, u1, u1m, diag));
+  }
+}
+
+// Per-chain complex dot sum conj(a) b (fermion.py:54-56); one CTA per (chain, slab).
+__global__ void k_spinor_dot(const double2* __restrict__ a, const double2* __restrict__ b,
+                             long long per_chain, int slabs, double* __restrict__ part) {
+  __shared__ double slot[2][32];
+  int c = blockIdx.y;
+  long long lo = per_chain * blockIdx.x / slabs, hi = per_chain * (blockIdx.x + 1) / slabs;
+  const double2* ac = a + (long long)c * per_chain;
+  const double2* bc = b + (long long)c * per_chain;
+  double re = 0.0, im = 0.0;
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    double2 x = __ldg(ac + i), y = __ldg(bc + i);
+    re += x.x * y.x + x.y * y.y;
+    im += x.x * y.y - x.y * y.x;
+  }
+  double sr = block_sum_rt(re, slot[0]);
+  double si = block_sum_rt(im, slot[1]);
+  if (threadIdx.x == 0) {
+    part[2 * ((long long)c * slabs + blockIdx.x)] = sr;
+    part[2 * ((long long)c * slabs + blockIdx.x) + 1] = si;
+  }
+}
+
+__global__ void k_spinor_dot_finish(const double* __restrict__ part, int slabs, double* __restrict__ out,
+                                    int B) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= B) return;
+  double re = 0.0, im = 0.0;
+  for (int k = 0; k < slabs; ++k) {
+    re += part[2 * ((long long)c * slabs + k)];
+    im += part[2 * ((long long)c * slabs + k) + 1];
+  }
+  out[2 * c] = re;
+  out[2 * c + 1] = im;
+}
+
+// A(n) = conj(w-(a)(n)) U_mu(n) w-(b)(n+mu);  B(n) = conj(w+(a)(n+mu)) conj(U_mu(n)) w+(b)(n)
+// (fermion.py:317-327), NumPy order: (conj(wa) * u) * wb.
+struct Bil {
+  double2 A, B;
+};
+template <int MU>
+__device__ __forceinline__ Bil bilinear(const Spinor& a_n, const Spinor& a_f, const Spinor& b_n,
+                                        const Spinor& b_f, double2 u) {
+  Bil r;
+  if (MU == 0) {
+    r.A = cmul(cmulc(wminus0(a_n), u), wminus0(b_f));
+    r.B = cmul(cmulc(wplus0(a_f), cconj(u)), wplus0(b_n));
+  } else {
+    r.A = cmul(cmulc(wminus1(a_n), u), wminus1(b_f));
+    r.B = cmul(cmulc(wplus1(a_f), cconj(u)), wplus1(b_n));
+  }
+  return r;
+}
+
+// Fermion force f = -Im(A - B) (fermion.py:330-336).  KICK: out = p - dt*(f [+ beta*g])
+// (kick_fermion / kick_full, integrators.py:172-186).
+template <bool KICK>
+__global__ void k_fermion_force(const double2* __restrict__ U, const double2* __restrict__ chi,
+                                const double2* __restrict__ xi, const double* __restrict__ q,
+                                double beta, const double* __restrict__ p, double dt,
+                                double* __restrict__ out, Geo g) {
+  long long n = (long long)g.B * g.V;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long b = i / g.V;
+    int s = (int)(i - b * g.V);
+    int x = s / g.T, t = s - x * g.T;
+    int xp = x + 1 == g.L ? 0 : x + 1, tp = t + 1 == g.T ? 0 : t + 1;
+    long long cb = b * g.V;
+    Spinor cn = ldg_spinor(chi, cb + s), xn = ldg_spinor(xi, cb + s);
+    Spinor cx = ldg_spinor(chi, cb + xp * g.T + t), xx = ldg_spinor(xi, cb + xp * g.T + t);
+    Spinor ct = ldg_spinor(chi, cb + x * g.T + tp), xt = ldg_spinor(xi, cb + x * g.T + tp);
+    const double2* Uc = U + 2 * cb;
+    Bil b0 = bilinear<0>(cn, cx, xn, xx, __ldg(Uc + s));
+    Bil b1 = bilinear<1>(cn, ct, xn, xt, __ldg(Uc + g.V + s));
+    double f0 = -(b0.A.y - b0.B.y);
+    double f1 = -(b1.A.y - b1.B.y);
+    long long o0 = 2 * cb + s, o1 = o0 + g.V;
+    if (KICK) {
+      if (q) {   // kick_full: force = gauge_force + fermion_force
+        int xm = x == 0 ? g.L - 1 : x - 1, tm = t == 0 ? g.T - 1 : t - 1;
+        const double* qc = q + 2 * cb;
+        double s0 = sin(plaq(qc, g.L, g.T, x, t));
+        double st = sin(plaq(qc, g.L, g.T, x, tm));
+        double sx = sin(plaq(qc, g.L, g.T, xm, t));
+        f0 = __dadd_rn(__dmul_rn(beta, __dsub_rn(s0, st)), f0);
+        f1 = __dadd_rn(__dmul_rn(beta, __dsub_rn(sx, s0)), f1);
+      }
+      out[o0] = __dsub_rn(p[o0], __dmul_rn(dt, f0));
+      out[o1] = __dsub_rn(p[o1], __dmul_rn(dt, f1));
+    } else {
+      out[o0] = f0;
+      out[o1] = f1;
+    }
+  }
+}
+
+// Weighted w-sums (fermion.py:362-383, Appendix A5), gather form per site.
+__global__ void k_wsums(const double2* __restrict__ U, const double* __restrict__ wt,
+                        const double2* __restrict__ chi, const double2* __restrict__ xi,
+                        double2* __restrict__ b1, double2* __restrict__ b2, Geo g) {
+  long long n = (long long)g.B * g.V;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long b = i / g.V;
+    int s = (int)(i - b * g.V);
+    int x = s / g.T, t = s - x * g.T;
+    long long cb = b * g.V;
+    const double2* Uc = U + 2 * cb;
+    const double* Wc = wt + 2 * cb;
+    double2 o10 = make_double2(0, 0), o11 = o10, o20 = o10, o21 = o10;
+#pragma unroll
+    for (int nu = 0; nu < 2; ++nu) {
+      int sf, sb;   // n + nu, n - nu
+      if (nu == 0) {
+        sf = (x + 1 == g.L ? 0 : x + 1) * g.T + t;
+        sb = (x == 0 ? g.L - 1 : x - 1) * g.T + t;
+      } else {
+        sf = x * g.T + (t + 1 == g.T ? 0 : t + 1);
+        sb = x * g.T + (t == 0 ? g.T - 1 : t - 1);
+      }
+      Spinor cb_ = ldg_spinor(chi, cb + sb), cf = ldg_spinor(chi, cb + sf);
+      Spinor xb = ldg_spinor(xi, cb + sb), xf = ldg_spinor(xi, cb + sf);
+      double2 un = __ldg(Uc + nu * g.V + s), ub = __ldg(Uc + nu * g.V + sb);
+      double wn = __ldg(Wc + nu * g.V + s), wb = __ldg(Wc + nu * g.V + sb);
+      double2 wm_cb = nu == 0 ? wminus0(cb_) : wminus1(cb_);
+      double2 wp_cf = nu == 0 ? wplus0(cf) : wplus1(cf);
+      double2 wm_xf = nu == 0 ? wminus0(xf) : wminus1(xf);
+      double2 wp_xb = nu == 0 ? wplus0(xb) : wplus1(xb);
+      // t1 = (0.5i * w*conj(U)*w-(chi))(n - nu)
+      double2 t1 = cscale(0.5, cmuli(cmul(cscale(wb, cconj(ub)), wm_cb)));
+      // t2 = -0.5i * w(n) U(n) w+(chi)(n + nu)
+      double2 t2 = cscale(-0.5, cmuli(cmul(cscale(wn, un), wp_cf)));
+      // t3 = -0.5i * w(n) U(n) w-(xi)(n + nu)
+      double2 t3 = cscale(-0.5, cmuli(cmul(cscale(wn, un), wm_xf)));
+      // t4 = (0.5i * w*conj(U)*w+(xi))(n - nu)
+      double2 t4 = cscale(0.5, cmuli(cmul(cscale(wb, cconj(ub)), wp_xb)));
+      o10 = cadd(o10, cadd(t1, t2));
+      o20 = cadd(o20, cadd(t3, t4));
+      if (nu == 0) {   // e- = -1, e+ = +1
+        o11 = cadd(o11, csub(t2, t1));
+        o21 = cadd(o21, csub(t4, t3));
+      } else {         // e- = -i, e+ = +i
+        o11 = cadd(o11, cmuli(csub(t2, t1)));
+        o21 = cadd(o21, cmuli(csub(t4, t3)));
+      }
+    }
+    long long o = cb + s;
+    b1[2 * o] = o10;
+    b1[2 * o + 1] = o11;
+    b2[2 * o] = o20;
+    b2[2 * o + 1] = o21;
+  }
+}
+
+// C = 2Im(A[z1,xi]-B[z1,xi]) + 2Im(A[chi,z2]-B[chi,z2]) - 2Re(A[chi,xi]+B[chi,xi])*w
+// (fermion.py:409-417)
+__global__ void k_fg_combine(const double2* __restrict__ U, const double2* __restrict__ z1,
+                             const double2* __restrict__ z2, const double2* __restrict__ chi,
+                             const double2* __restrict__ xi, const double* __restrict__ wt,
+                             double* __restrict__ out, Geo g) {
+  long long n = (long long)g.B * g.V;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long b = i / g.V;
+    int s = (int)(i - b * g.V);
+    int x = s / g.T, t = s - x * g.T;
+    long long cb = b * g.V;
+    const double2* Uc = U + 2 * cb;
+#pragma unroll
+    for (int mu = 0; mu < 2; ++mu) {
+      int sf = mu == 0 ? (x + 1 == g.L ? 0 : x + 1) * g.T + t : x * g.T + (t + 1 == g.T ? 0 : t + 1);
+      Spinor z1n = ldg_spinor(z1, cb + s), z1f = ldg_spinor(z1, cb + sf);
+      Spinor z2n = ldg_spinor(z2, cb + s), z2f = ldg_spinor(z2, cb + sf);
+      Spinor cn = ldg_spinor(chi, cb + s), cf = ldg_spinor(chi, cb + sf);
+      Spinor xn = ldg_spinor(xi, cb + s), xf = ldg_spinor(xi, cb + sf);
+      double2 u = __ldg(Uc + mu * g.V + s);
+      Bil a1 = mu == 0 ? bilinear<0>(z1n, z1f, xn, xf, u) : bilinear<1>(z1n, z1f, xn, xf, u);
+      Bil a2 = mu == 0 ? bilinear<0>(cn, cf, z2n, z2f, u) : bilinear<1>(cn, cf, z2n, z2f, u);
+      Bil a3 = mu == 0 ? bilinear<0>(cn, cf, xn, xf, u) : bilinear<1>(cn, cf, xn, xf, u);
+      double w = __ldg(wt + 2 * cb + mu * g.V + s);
+      double v = 2.0 * (a1.A.y - a1.B.y) + 2.0 * (a2.A.y - a2.B.y) - 2.0 * (a3.A.x + a3.B.x) * w;
+      out[2 * cb + mu * g.V + s] = v;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int sch_links_to_u(sch_ctx* ctx, const double* q, double* U, int B, int L, int T, int fermion_bc) {
+  SCH_CHECK_ARG(ctx, q && U && B >= 1 && L >= 2 && T >= 2, "links_to_u: bad args");
+  SCH_CHECK_ARG(ctx, fermion_bc == 0 || fermion_bc == 1, "links_to_u: fermion_bc must be 0 or 1");
+  Geo g{B, L, T, (long long)L * T};
+  k_links_to_u<<<grid_for((long long)B * 2 * g.V), 256, 0, ctx->stream>>>(q, (double2*)U, g,
+                                                                         fermion_bc);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+int sch_dslash(sch_ctx* ctx, const double* U, int u_batched, const double* psi, double* out, int B,
+               int L, int T, double m0, int dagger) {
+  SCH_CHECK_ARG(ctx, U && psi && out && B >= 1 && L >= 2 && T >= 2, "dslash: bad args");
+  SCH_CHECK_ARG(ctx, psi != out, "dslash: in-place application is not supported");
+  Geo g{B, L, T, (long long)L * T};
+  long long us = u_batched ? 2 * g.V : 0;
+  unsigned grid = grid_for((long long)B * g.V);
+  if (dagger)
+    k_dslash<true><<<grid, 256, 0, ctx->stream>>>((const double2*)U, us, (const double2*)psi,
+                                                   (double2*)out, g, 2.0 + m0);
+  else
+    k_dslash<false><<<grid, 256, 0, ctx->stream>>>((const double2*)U, us, (const double2*)psi,
+                                                    (double2*)out, g, 2.0 + m0);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+int sch_ddagd(sch_ctx* ctx, const double* U, const double* psi, double* out, int B, int L, int T,
+              double m0) {
+  SCH_CHECK_ARG(ctx, U && psi && out && B >= 1 && L >= 2 && T >= 2, "ddagd: bad args");
+  SCH_CHECK_ARG(ctx, psi != out, "ddagd: in-place application is not supported");
+  TileShape sh = pick_tile(L, T);
+  TileArgs a{};
+  a.U = (const double2*)U;
+  a.in = (const double2*)psi;
+  a.out = (double2*)out;
+  a.B = B;
+  a.L = L;
+  a.T = T;
+  a.tiles_t = sh.tiles_t;
+  a.tiles_per_chain = sh.tiles_x * sh.tiles_t;
+  a.diag = 2.0 + m0;
+  launch_normal_tile<MODE_PLAIN>(sh, a, ctx->stream);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+int sch_spinor_dot(sch_ctx* ctx, const double* a, const double* b, double* out, int B, long long V) {
+  SCH_CHECK_ARG(ctx, a && b && out && B >= 1 && V >= 1, "spinor_dot: bad args");
+  long long per_chain = 2 * V;   // complex entries per chain
+  int slabs = (int)((per_chain + 16383) / 16384);
+  if (slabs > 256) slabs = 256;
+  void* ws;
+  int st = sch_workspace(ctx, sizeof(double) * 2 * (size_t)B * slabs, &ws);
+  if (st) return st;
+  k_spinor_dot<<<dim3(slabs, B), 256, 0, ctx->stream>>>((const double2*)a, (const double2*)b,
+                                                         per_chain, slabs, (double*)ws);
+  SCH_LAUNCHED(ctx);
+  k_spinor_dot_finish<<<blocks_for(B, 128), 128, 0, ctx->stream>>>((const double*)ws, slabs, out, B);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+int sch_fermion_force(sch_ctx* ctx, const double* U, const double* chi, const double* xi,
+                      double* out, int B, int L, int T) {
+  SCH_CHECK_ARG(ctx, U && chi && xi && out && B >= 1 && L >= 2 && T >= 2, "fermion_force: bad args");
+  Geo g{B, L, T, (long long)L * T};
+  k_fermion_force<false><<<grid_for((long long)B * g.V), 256, 0, ctx->stream>>>(
+      (const double2*)U, (const double2*)chi, (const double2*)xi, nullptr, 0.0, nullptr, 0.0, out, g);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+int sch_kick_fermion(sch_ctx* ctx, const double* U, const double* chi, const double* xi,
+                     const double* q, double beta, const double* p, double dt, double* p_out, int B,
+                     int L, int T) {
+  SCH_CHECK_ARG(ctx, U && chi && xi && p && p_out && B >= 1 && L >= 2 && T >= 2,
+                "kick_fermion: bad args");
+  Geo g{B, L, T, (long long)L * T};
+  k_fermion_force<true><<<grid_for((long long)B * g.V), 256, 0, ctx->stream>>>(
+      (const double2*)U, (const double2*)chi, (const double2*)xi, q, beta, p, dt, p_out, g);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+int sch_weighted_w_sums(sch_ctx* ctx, const double* U, const double* weight, const double* chi,
+                        const double* xi, double* b1, double* b2, int B, int L, int T) {
+  SCH_CHECK_ARG(ctx, U && weight && chi && xi && b1 && b2 && B >= 1 && L >= 2 && T >= 2,
+                "weighted_w_sums: bad args");
+  Geo g{B, L, T, (long long)L * T};
+  k_wsums<<<grid_for((long long)B * g.V), 256, 0, ctx->stream>>>(
+      (const double2*)U, weight, (const double2*)chi, (const double2*)xi, (double2*)b1, (double2*)b2, g);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+int sch_fg_fermion_combine(sch_ctx* ctx, const double* U, const double* z1, const double* z2,
+                           const double* chi, const double* xi, const double* weight, double* out,
+                           int B, int L, int T) {
+  SCH_CHECK_ARG(ctx, U && z1 && z2 && chi && xi && weight && out && B >= 1 && L >= 2 && T >= 2,
+                "fg_fermion_combine: bad args");
+  Geo g{B, L, T, (long long)L * T};
+  k_fg_combine<<<grid_for((long long)B * g.V), 256, 0, ctx->stream>>>(
+      (const double2*)U, (const double2*)z1, (const double2*)z2, (const double2*)chi,
+      (const double2*)xi, weight, out, g);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+}  // extern "C"

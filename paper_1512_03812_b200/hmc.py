@@ -1,0 +1,247 @@
+"""HMC update cycle on the B200: heatbaths, trajectory, Hamiltonian,
+Metropolis; the batched fixed-start |dH| measurement; thermalization; and the
+independent-chain ensemble update used by the benchmark.
+
+Mirror of ``schwinger.hmc`` (pkg/src/schwinger/hmc.py).  ``hmc_update`` and
+``measure_dh`` keep the reference signatures, draw order and return types
+(dH as a Python float, reject returns the caller's original object).
+``hmc_update_ensemble`` is the B200 addition: B chains advanced together with
+per-chain CG stopping, per-chain RNG streams and per-chain Metropolis — the
+same result as B independent ``hmc_update`` calls.
+"""
+
+from __future__ import annotations
+
+import logging
+import time
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import HmcConfig
+from .fermion import InversionCounter, WilsonDirac, draw_phi, pseudofermion_heatbath, spinor_dot
+from .gauge import avg_plaquette, gauge_action
+from .integrators import IntegratorSpec, MdState, integrate_trajectory
+from .lattice import (DeviceRng, LatticeGeom, as_links, as_spinor, cold_start, kinetic_energy,
+                      sample_momenta)
+
+log = logging.getLogger("schwinger")
+
+
+@dataclass(frozen=True)
+class TrajectoryStats:
+    dh: float
+    accepted: bool
+    inversions: int
+    n_steps: int
+    wall_time: float
+
+
+@dataclass(frozen=True)
+class DhMeasurement:
+    """|dH| statistics over independent trajectories from one configuration."""
+
+    dh: np.ndarray
+    mean_abs: float
+    stderr: float
+    acceptance: float
+    inversions_per_traj: int
+    n_steps: int
+    wall_per_traj: float
+
+
+@dataclass(frozen=True)
+class EnsembleStats:
+    """Per-chain outcome of one ensemble trajectory."""
+
+    dh: np.ndarray
+    accepted: np.ndarray
+    inversions: int          # per chain, reference convention
+    n_steps: int
+    wall_time: float
+
+
+def hamiltonian(state: MdState) -> torch.Tensor:
+    """H = (1/2) sum p^2 + S_G + S_F per chain; one normal solve, shared with
+    an adjacent kick at the same links when ``reuse_solves`` (hmc.py:44-51)."""
+    kin = kinetic_energy(state.p)
+    s_g = gauge_action(state.q, state.beta)
+    _, _, xi = state.solve_pair()
+    s_f = spinor_dot(state.eta, xi).real
+    return (kin + s_g) + s_f
+
+
+def metropolis(dh: float, rng) -> bool:
+    """Accept with probability min(1, exp(-dH)); draws only when dH > 0 (hmc.py:54-60)."""
+    if not np.isfinite(dh):
+        raise ValueError(f"non-finite energy change {dh}")
+    if dh <= 0.0:
+        return True
+    return bool(rng.random() < np.exp(-dh))
+
+
+def _spec_of(config: HmcConfig) -> IntegratorSpec:
+    return IntegratorSpec(scheme=config.scheme, h=config.h, micro_per_call=config.micro_per_call,
+                          micro_ratio=config.micro_ratio)
+
+
+def _sync():
+    torch.cuda.synchronize()
+
+
+def hmc_update(q, config: HmcConfig, rng, counter: InversionCounter | None = None,
+               reuse_solves: bool = True):
+    """One HMC update (hmc.py:69-95); returns (links, TrajectoryStats).
+
+    On rejection the caller's object is handed back untouched."""
+    counter = counter if counter is not None else InversionCounter()
+    geom = LatticeGeom(config.L, config.T)
+    q_dev = as_links(q)
+    p = sample_momenta(rng, geom)
+    if config.quenched:
+        eta = torch.zeros(geom.spinor_shape(), dtype=torch.complex128, device=q_dev.device)
+    else:
+        eta = pseudofermion_heatbath(WilsonDirac(q_dev, config.m0, config.fermion_bc), rng)
+    state = MdState(q=q_dev.clone(), p=p, eta=eta, beta=config.beta, m0=config.m0,
+                    tol=config.cg_tol, counter=counter, fermion_bc=config.fermion_bc,
+                    stop="per_chain", reuse_solves=reuse_solves)
+    h_start = hamiltonian(state)
+    _sync()
+    t0 = time.perf_counter()
+    result = integrate_trajectory(state, _spec_of(config), config.tau)
+    _sync()
+    wall = time.perf_counter() - t0
+    h_end = hamiltonian(state)
+    state.check_solves()
+    dh = float((h_end - h_start).item())
+    accepted = metropolis(dh, rng)
+    stats = TrajectoryStats(dh=dh, accepted=accepted, inversions=result.inversions,
+                            n_steps=result.n_steps, wall_time=wall)
+    return (state.q if accepted else q), stats
+
+
+def measure_dh(q0, config: HmcConfig, rng, n_samples: int | None = None,
+               reuse_solves: bool = True) -> DhMeasurement:
+    """Mean |dH| over n independent momentum/pseudofermion draws from one
+    configuration, evolved as one batch with global CG stopping; no
+    Metropolis step (hmc.py:98-130)."""
+    n = n_samples if n_samples is not None else config.n_samples
+    geom = LatticeGeom(config.L, config.T)
+    counter = InversionCounter()
+    q0 = as_links(q0)
+    p = sample_momenta(rng, geom, batch=n)
+    if config.quenched:
+        eta = torch.zeros(geom.spinor_shape(n), dtype=torch.complex128, device=q0.device)
+    else:
+        eta = pseudofermion_heatbath(WilsonDirac(q0, config.m0, config.fermion_bc), rng, batch=n)
+    q = q0.expand((n,) + tuple(q0.shape)).contiguous()
+    state = MdState(q=q, p=p, eta=eta, beta=config.beta, m0=config.m0, tol=config.cg_tol,
+                    counter=counter, fermion_bc=config.fermion_bc, stop="batch_global",
+                    reuse_solves=reuse_solves)
+    h_start = hamiltonian(state)
+    _sync()
+    t0 = time.perf_counter()
+    result = integrate_trajectory(state, _spec_of(config), config.tau)
+    _sync()
+    wall = time.perf_counter() - t0
+    h_end = hamiltonian(state)
+    state.check_solves()
+    dh = (h_end - h_start).cpu().numpy().astype(np.float64)
+    ad = np.abs(dh)
+    mean_abs = float(np.mean(ad))
+    stderr = float(np.std(ad, ddof=1) / np.sqrt(n)) if n > 1 else 0.0
+    acceptance = float(np.mean(np.minimum(1.0, np.exp(-dh))))
+    return DhMeasurement(dh=dh, mean_abs=mean_abs, stderr=stderr, acceptance=acceptance,
+                         inversions_per_traj=result.inversions, n_steps=result.n_steps,
+                         wall_per_traj=wall / n)
+
+
+def thermalize(config: HmcConfig, rng):
+    """Cold start + n_thermalize leapfrog updates with step annealing
+    (hmc.py:133-155).  Returns (links on the device, plaquette history)."""
+    geom = LatticeGeom(config.L, config.T)
+    q = cold_start(geom)
+    tc = replace(config, scheme="leapfrog", h=min(config.h, 0.1), micro_per_call=None)
+    block, hits, history = 20, 0, []
+    for i in range(config.n_thermalize):
+        q, stats = hmc_update(q, tc, rng)
+        hits += stats.accepted
+        history.append(float(avg_plaquette(q).item()))
+        if (i + 1) % block == 0:
+            if hits < 0.8 * block:
+                tc = replace(tc, h=tc.h * 0.7)
+                log.info("thermalize: lowering step size to %.4g", tc.h)
+            hits = 0
+    return q, history
+
+
+# ---------------------------------------------------------------------------
+# chain ensemble (BASELINE configs 3-4)
+# ---------------------------------------------------------------------------
+
+def hmc_update_ensemble(q, config: HmcConfig, rngs=None, device_rng: DeviceRng | None = None,
+                        counter: InversionCounter | None = None, reuse_solves: bool = True):
+    """Advance B independent chains by one HMC update each.
+
+    ``q`` is (B, 2, L, T).  Parity mode: ``rngs`` is a list of B NumPy
+    generators (chain c == ``make_rng(seed, stream=c)``) and every chain sees
+    exactly the draws an unbatched ``hmc_update`` would make.  Bench mode:
+    ``device_rng`` draws momenta, pseudofermions and Metropolis uniforms on
+    the GPU.  Returns (links, EnsembleStats)."""
+    q = as_links(q)
+    if q.ndim != 4:
+        raise ValueError("hmc_update_ensemble expects links of shape (B, 2, L, T)")
+    B = q.shape[0]
+    geom = LatticeGeom(config.L, config.T)
+    counter = counter if counter is not None else InversionCounter()
+    if (rngs is None) == (device_rng is None):
+        raise ValueError("pass exactly one of rngs (parity mode) or device_rng (bench mode)")
+    if rngs is not None:
+        if len(rngs) != B:
+            raise ValueError(f"need one generator per chain ({B}), got {len(rngs)}")
+        ps, phis = [], []
+        for r in rngs:
+            ps.append(r.standard_normal(geom.links_shape()))
+            if not config.quenched:
+                phis.append(draw_phi(r, config.L, config.T))
+        p = as_links(np.stack(ps))
+        phi = as_spinor(np.stack(phis)) if phis else None
+    else:
+        p = device_rng.normal(B, geom.links_shape())
+        phi = None if config.quenched else device_rng.complex_normal(B, geom.spinor_shape(),
+                                                                     1.0 / np.sqrt(2.0))
+    if config.quenched:
+        eta = torch.zeros(geom.spinor_shape(B), dtype=torch.complex128, device=q.device)
+    else:
+        eta = WilsonDirac(q, config.m0, config.fermion_bc).apply_dag(phi)
+    state = MdState(q=q.clone(), p=p, eta=eta, beta=config.beta, m0=config.m0, tol=config.cg_tol,
+                    counter=counter, fermion_bc=config.fermion_bc, stop="per_chain",
+                    reuse_solves=reuse_solves)
+    t0 = time.perf_counter()
+    h_start = hamiltonian(state)
+    result = integrate_trajectory(state, _spec_of(config), config.tau)
+    h_end = hamiltonian(state)
+    dh_dev = h_end - h_start
+    if device_rng is not None:
+        u = device_rng.uniform(B)
+        acc = torch.empty((B,), dtype=torch.int32, device=q.device)
+        _lib.ctx().call("sch_metropolis", _lib.ptr(dh_dev), _lib.ptr(u), _lib.ptr(acc), B)
+        state.check_solves()
+        dh = dh_dev.cpu().numpy()
+        acc_h = acc.cpu().numpy()
+        if (acc_h < 0).any():
+            raise ValueError(f"non-finite energy change {dh[acc_h < 0][0]}")
+        accepted = acc_h == 1
+    else:
+        state.check_solves()
+        dh = dh_dev.cpu().numpy()
+        accepted = np.array([metropolis(float(d), r) for d, r in zip(dh, rngs)], dtype=bool)
+        acc = torch.from_numpy(accepted.astype(np.int32)).to(q.device)
+    out = torch.empty_like(q)
+    _lib.ctx().call("sch_select_chains", _lib.ptr(acc), _lib.ptr(state.q), _lib.ptr(q),
+                    _lib.ptr(out), B, q[0].numel())
+    wall = time.perf_counter() - t0
+    return out, EnsembleStats(dh=dh, accepted=accepted, inversions=result.inversions,
+                              n_steps=result.n_steps, wall_time=wall)

@@ -1,0 +1,268 @@
+"""Geometry, RNG streams, link/momentum updates and gauge-config I/O.
+
+Mirror of the reference ``schwinger.lattice`` (pkg/src/schwinger/lattice.py)
+with fields resident on the B200: link-type fields are float64 CUDA tensors
+of shape (..., 2, L, T), spinors complex128 CUDA tensors (..., L, T, 2) —
+the reference's own layouts (lattice.py:3-12), so no conversion happens at
+the boundary.  Every arithmetic operation runs in the sm_100a library; torch
+only allocates and moves memory.
+
+Random draws keep the reference convention (NumPy Philox keyed by
+[seed, stream], lattice.py:86-89) and are drawn on the host in the
+reference's order, then uploaded ("parity mode").  ``DeviceRng`` is the
+bench-mode alternative that draws on the GPU.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+
+TWO_PI = 2.0 * np.pi
+
+LINK_X, LINK_T = -2, -1
+SPIN_X, SPIN_T = -3, -2
+
+
+# ---------------------------------------------------------------------------
+# tensor plumbing
+# ---------------------------------------------------------------------------
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise _lib.NativeUnavailable("no CUDA device: the B200 path has no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def as_links(a) -> torch.Tensor:
+    """float64 CUDA tensor (..., 2, L, T), contiguous."""
+    if isinstance(a, torch.Tensor):
+        t = a
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64))
+    return t.to(device=device(), dtype=torch.float64).contiguous()
+
+
+def as_spinor(a) -> torch.Tensor:
+    """complex128 CUDA tensor (..., L, T, 2), contiguous."""
+    if isinstance(a, torch.Tensor):
+        t = a
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(a, dtype=np.complex128))
+    return t.to(device=device(), dtype=torch.complex128).contiguous()
+
+
+def to_numpy(t) -> np.ndarray:
+    if isinstance(t, torch.Tensor):
+        return t.detach().cpu().numpy()
+    return np.asarray(t)
+
+
+def n_chains(t: torch.Tensor, core_dims: int = 3) -> int:
+    """Number of chains in the leading batch dims (1 for an unbatched field)."""
+    b = 1
+    for d in t.shape[:-core_dims]:
+        b *= d
+    return b
+
+
+def squeeze_chain(v: torch.Tensor, like: torch.Tensor, core_dims: int = 3) -> torch.Tensor:
+    """Shape a per-chain vector (B,) like the batch dims of ``like`` (0-d if unbatched)."""
+    return v.reshape(like.shape[:-core_dims])
+
+
+def wrap_angles(q):
+    """Reduce angles to [-pi, pi) (lattice.py:28-30)."""
+    q = as_links(q)
+    out = torch.empty_like(q)
+    _lib.ctx().call("sch_wrap_angles", _lib.ptr(q), _lib.ptr(out), q.numel())
+    return out
+
+
+@dataclass(frozen=True)
+class LatticeGeom:
+    """Lattice extents, L sites in space and T in time (lattice.py:33-74)."""
+
+    L: int
+    T: int
+
+    def __post_init__(self):
+        if self.L < 2 or self.T < 2:
+            raise ValueError(f"hopping stencils need L, T >= 2, got {self.L}x{self.T}")
+
+    @property
+    def volume(self) -> int:
+        return self.L * self.T
+
+    @property
+    def n_links(self) -> int:
+        return 2 * self.volume
+
+    def site_index(self, x: int, t: int) -> int:
+        return t * self.L + x
+
+    def site_coords(self, idx: int) -> tuple[int, int]:
+        return idx % self.L, idx // self.L
+
+    def shift_site(self, site, mu: int, s: int):
+        x, t = site
+        if mu == 0:
+            return (x + s) % self.L, t
+        if mu == 1:
+            return x, (t + s) % self.T
+        raise ValueError(f"direction must be 0 or 1, got {mu}")
+
+    def links_shape(self, batch: int | None = None):
+        return (2, self.L, self.T) if batch is None else (batch, 2, self.L, self.T)
+
+    def spinor_shape(self, batch: int | None = None):
+        return (self.L, self.T, 2) if batch is None else (batch, self.L, self.T, 2)
+
+
+def geom_of(field) -> LatticeGeom:
+    return LatticeGeom(int(field.shape[-2]), int(field.shape[-1]))
+
+
+# ---------------------------------------------------------------------------
+# random streams (host, reference convention)
+# ---------------------------------------------------------------------------
+
+def make_rng(seed: int, stream: int = 0) -> np.random.Generator:
+    """Counter-based generator keyed by [seed, stream] (lattice.py:86-89)."""
+    key = np.array([seed % 2**64, stream % 2**64], dtype=np.uint64)
+    return np.random.Generator(np.random.Philox(key=key))
+
+
+def sample_momenta(rng, geom: LatticeGeom, batch: int | None = None) -> torch.Tensor:
+    """Gaussian momenta, drawn with the reference generator (lattice.py:92-95)."""
+    return as_links(rng.standard_normal(geom.links_shape(batch)))
+
+
+def cold_start(geom: LatticeGeom, batch: int | None = None) -> torch.Tensor:
+    return torch.zeros(geom.links_shape(batch), dtype=torch.float64, device=device())
+
+
+def hot_start(rng, geom: LatticeGeom, batch: int | None = None) -> torch.Tensor:
+    """theta ~ U(-pi, pi) (lattice.py:102-104)."""
+    return as_links(rng.uniform(-np.pi, np.pi, size=geom.links_shape(batch)))
+
+
+class DeviceRng:
+    """Bench-mode generator: Philox4x32-10 on the GPU, one stream per chain
+    (key = (seed, stream0 + chain)), advancing a per-draw counter.  Not
+    value-identical to the reference's NumPy stream."""
+
+    def __init__(self, seed: int, stream0: int = 0):
+        self.seed = int(seed) % 2**64
+        self.stream0 = int(stream0) % 2**64
+        self.counter = 0
+
+    def normal(self, n_chains: int, shape, scale: float = 1.0) -> torch.Tensor:
+        out = torch.empty((n_chains,) + tuple(shape), dtype=torch.float64, device=device())
+        per = out.numel() // n_chains
+        _lib.ctx().call("sch_rng_normal", _lib.ptr(out), n_chains, per, self.seed, self.stream0,
+                        self.counter, float(scale))
+        self.counter += 1
+        return out
+
+    def complex_normal(self, n_chains: int, shape, scale: float) -> torch.Tensor:
+        """complex128 field whose re/im parts are iid scale*N(0,1)."""
+        out = torch.empty((n_chains,) + tuple(shape), dtype=torch.complex128, device=device())
+        per = 2 * (out.numel() // n_chains)
+        _lib.ctx().call("sch_rng_normal", _lib.ptr(out), n_chains, per, self.seed, self.stream0,
+                        self.counter, float(scale))
+        self.counter += 1
+        return out
+
+    def uniform(self, n_chains: int) -> torch.Tensor:
+        out = torch.empty((n_chains,), dtype=torch.float64, device=device())
+        _lib.ctx().call("sch_rng_uniform", _lib.ptr(out), n_chains, 1, self.seed, self.stream0,
+                        self.counter)
+        self.counter += 1
+        return out
+
+
+# ---------------------------------------------------------------------------
+# elementary updates (device)
+# ---------------------------------------------------------------------------
+
+def rotate_links(q, p, h: float) -> torch.Tensor:
+    """Group-exact drift q -> wrap(q + h p) (lattice.py:111-118)."""
+    q, p = as_links(q), as_links(p)
+    if q.shape != p.shape:
+        q, p = torch.broadcast_tensors(q, p)
+        q, p = q.contiguous(), p.contiguous()
+    out = torch.empty_like(q)
+    _lib.ctx().call("sch_rotate_links", _lib.ptr(q), _lib.ptr(p), float(h), _lib.ptr(out), q.numel())
+    return out
+
+
+def shift_momenta(p, force, h: float) -> torch.Tensor:
+    """p -> p - h*force (lattice.py:121-125)."""
+    p, force = as_links(p), as_links(force)
+    if p.shape[-3:] != force.shape[-3:]:
+        raise ValueError(f"shape mismatch: momenta {tuple(p.shape)} vs force {tuple(force.shape)}")
+    return kick(p, force, h)
+
+
+def kick(p: torch.Tensor, f: torch.Tensor, a: float, g: torch.Tensor | None = None,
+         c: float = 0.0) -> torch.Tensor:
+    """out = p - (a*f + c*g), or p - a*f without g (NumPy operation order)."""
+    if p.shape != f.shape or (g is not None and g.shape != p.shape):
+        shape = torch.broadcast_shapes(p.shape, f.shape, *(() if g is None else (g.shape,)))
+        p = p.expand(shape).contiguous()
+        f = f.expand(shape).contiguous()
+        g = None if g is None else g.expand(shape).contiguous()
+    out = torch.empty_like(p)
+    _lib.ctx().call("sch_kick", _lib.ptr(p), _lib.ptr(f), float(a), _lib.ptr(g), float(c),
+                    _lib.ptr(out), p.numel())
+    return out
+
+
+def kinetic_energy(p) -> torch.Tensor:
+    """(1/2) sum p^2 per chain (lattice.py:128-130); 0-d for an unbatched field."""
+    p = as_links(p)
+    B = n_chains(p)
+    out = torch.empty((B,), dtype=torch.float64, device=p.device)
+    _lib.ctx().call("sch_kinetic_energy", _lib.ptr(p), _lib.ptr(out), B, p.numel() // B)
+    return squeeze_chain(out, p)
+
+
+# ---------------------------------------------------------------------------
+# gauge configuration files (lattice.py:137-172 format)
+# ---------------------------------------------------------------------------
+
+_MAGIC = "schwinger-u1 v1"
+
+
+def save_gauge_config(path, q, beta: float, m0: float, seed: int) -> None:
+    """ASCII header + 2V little-endian float64, site-major (t-major), directions
+    interleaved; bit-exact round trip (lattice.py:140-154)."""
+    q = to_numpy(q)
+    if q.ndim != 3:
+        raise ValueError("config files hold a single (2, L, T) configuration")
+    g = geom_of(q)
+    head = f"{_MAGIC} {g.L} {g.T} {beta!r} {m0!r} {seed}\n".encode("ascii")
+    body = np.ascontiguousarray(np.transpose(q, (2, 1, 0)), dtype="<f8").tobytes()
+    with open(path, "wb") as fh:
+        fh.write(head + body)
+
+
+def load_gauge_config(path, to_device: bool = False):
+    """Read a 'schwinger-u1 v1' file (lattice.py:157-172); host array by default."""
+    with open(path, "rb") as fh:
+        head = fh.readline().decode("ascii").strip()
+        body = fh.read()
+    parts = head.split()
+    if len(parts) != 7 or " ".join(parts[:2]) != _MAGIC:
+        raise ValueError(f"{path}: not a schwinger-u1 v1 configuration (header {head!r})")
+    L, T = int(parts[2]), int(parts[3])
+    meta = {"L": L, "T": T, "beta": float(parts[4]), "m0": float(parts[5]), "seed": int(parts[6])}
+    if len(body) != 2 * L * T * 8:
+        raise ValueError(f"{path}: expected {2 * L * T * 8} payload bytes, got {len(body)}")
+    q = np.ascontiguousarray(np.frombuffer(body, dtype="<f8").reshape(T, L, 2).transpose(2, 1, 0))
+    return (as_links(q) if to_device else q), meta
