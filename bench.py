@@ -1,0 +1,448 @@
+#!/usr/bin/env python
+"""Benchmark: HMC chain-trajectories/s of the Schwinger-model ensemble on B200.
+
+Workload (BASELINE.json configs[2], "cfg3"): independent 16x16 chains,
+beta=2.0, m0=0.1, tau=1, adapted nested force-gradient (the paper's scheme),
+micro_per_call=2, CG tolerance 1e-10, complex128, hot start; 8192 chains per
+GPU (weak scaling across ranks, no collective on the data path; one NCCL
+all-gather of per-chain dH/accept at the end).  A "step" is one full HMC
+update of every chain (heatbaths, H, trajectory, H, Metropolis).
+
+Also reported on the same line:
+  roofline   : the dominant kernel (the resident per-chain CG) against the
+               HBM roofline on the SURVEY §8(d) algorithmic model (352 B per
+               site per CG iteration) — "effective", since the CG working set
+               lives in shared memory/registers — plus its FP64 rate against
+               a live FP64 FMA probe;
+  stencil    : BASELINE configs[1] ("cfg2"): 4096 x 32^2, fused D^dag D GB/s at
+               96 B/site and the streaming CG to 1e-10 at 352 B/site/iteration;
+  cpu_baseline: the CPU oracle port (per-chain hmc_update) on the host cores;
+  e2e        : the same metric through the public API with the links copied
+               host->device and device->host every step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_PATH = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM = 6650.0
+
+CFG3 = dict(L=16, T=16, beta=2.0, m0=0.1, tau=1.0, scheme="adapted-nested-fg", micro_per_call=2,
+            cg_tol=1e-10)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--chains", type=int, default=8192, help="chains per GPU")
+    ap.add_argument("--outer", type=int, default=4, help="outer (fermion) steps per trajectory")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-stencil", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        d = json.loads(PEAKS_PATH.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline and --impl reference): per-chain unbatched
+# hmc_update of the CPU port, one process per host core.
+# ---------------------------------------------------------------------------
+
+def _cpu_cfg(outer):
+    from oracle import schwinger_oracle as O
+    return O.Config(h=1.0 / outer, **CFG3)
+
+
+def _cpu_chain_worker(args):
+    seed, stream, seconds, outer = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import schwinger_oracle as O
+    cfg = _cpu_cfg(outer)
+    rng = O.make_rng(seed, stream)
+    q = O.hot_start(rng, cfg.L, cfg.T)
+    n, t0 = 0, time.perf_counter()
+    while True:
+        q, _ = O.hmc_update(q, cfg, rng)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return n, el
+
+
+def _cpu_one_traj(args):
+    seed, stream, outer = args
+    from oracle import schwinger_oracle as O
+    cfg = _cpu_cfg(outer)
+    rng = O.make_rng(seed, stream)
+    q = O.hot_start(rng, cfg.L, cfg.T)
+    t0 = time.perf_counter()
+    O.hmc_update(q, cfg, rng)
+    return time.perf_counter() - t0
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(seconds, outer):
+    cores = cpu_cores()
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_cpu_chain_worker, [(1234, c, seconds, outer) for c in range(cores)])
+    n = sum(r[0] for r in res)
+    rate = sum(r[0] / r[1] for r in res)
+    return {"value": rate, "unit": "chain-trajectories/s", "cores": cores, "kind": "port",
+            "sample": f"{n} unbatched hmc_update trajectories of independent 16x16 hot-start "
+                      f"chains (cfg3 physics, adapted-nested-fg, {outer}x2 steps, tol 1e-10), "
+                      f"{cores} processes x {seconds:.0f}s, oracle/schwinger_oracle.py"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU port of the reference path on all host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return 0
+    cores = cpu_cores()
+    ctx = mp.get_context("fork")
+    times = []
+    with ctx.Pool(cores) as pool:
+        for step in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            pool.map(_cpu_one_traj, [(99, step * cores + c, args.outer) for c in range(cores)])
+            if step >= args.warmup:
+                times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    value = cores / t
+    line = {
+        "impl": "reference", "metric": "HMC trajectories/s", "value": value,
+        "unit": "chain-trajectories/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic",
+        "config": {"workload": "cfg3: independent 16x16 chains, beta=2.0, m0=0.1, tau=1, "
+                               f"adapted-nested-fg {args.outer}x2 steps, tol 1e-10, hot start",
+                   "chains_per_step": cores},
+        "cpu_baseline": {"value": value, "unit": "chain-trajectories/s", "cores": cores,
+                         "kind": "port",
+                         "sample": f"each step: {cores} processes x 1 unbatched hmc_update "
+                                   "trajectory (oracle/schwinger_oracle.py; the reference is "
+                                   "pure Python, so the port is the runnable reference path)"},
+        "e2e": {"value": value, "unit": "chain-trajectories/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nme, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(nme)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def fp64_probe(torch, _lib):
+    blocks, iters = 148 * 16, 4096
+    scratch = torch.empty((blocks,), dtype=torch.float64, device="cuda")
+    ctx = _lib.ctx()
+    ctx.call("sch_probe_fp64", _lib.ptr(scratch), blocks, 64)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ctx.call("sch_probe_fp64", _lib.ptr(scratch), blocks, iters)
+        e1.record()
+        torch.cuda.synchronize()
+        flops = blocks * 256.0 * iters * 64
+        best = max(best, flops / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
+def stencil_bench(torch, sw, _lib, hbm_peak):
+    """cfg2: 4096 x 32^2, fused D^dag D and the CG to 1e-10."""
+    from paper_1512_03812_b200 import fermion as F
+    B, L = 4096, 32
+    V = L * L
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(2)
+    q = (torch.rand((B, 2, L, L), dtype=torch.float64, device="cuda", generator=gen) * 2 - 1) * math.pi
+    psi = torch.randn((B, L, L, 2), dtype=torch.complex128, device="cuda", generator=gen)
+    op = sw.WilsonDirac(q, 0.1)
+    out = op.normal(psi)
+    torch.cuda.synchronize()
+    reps = 20
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        op.normal(psi)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / reps * 1e-3
+    sites = B * V
+    ddd_gbs = 96.0 * sites / t / 1e9
+    res = {"workload": "cfg2: 4096 x 32x32, m0=0.1, complex128",
+           "ddagd": {"achieved": ddd_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": ddd_gbs / hbm_peak, "us_per_application": t * 1e6,
+                     "bytes_model": "96 B/site (psi in + U + out)",
+                     "kernel": "k_normal_tile<8,32,2,0,PLAIN>"}}
+    # CG, both engines
+    for mode, label in (("per_chain", "resident"), ("batch_global", "streaming")):
+        F.CG_PROFILE = []
+        x, info = F.cg_solve(op, psi, 1e-10, stop=mode)
+        torch.cuda.synchronize()
+        prof, F.CG_PROFILE = F.CG_PROFILE, None
+        ev0, ev1, iters, vv = prof[0]
+        ms = ev0.elapsed_time(ev1)
+        tot_it = int(iters.sum().item()) if mode == "per_chain" else int(iters.max().item()) * B
+        gbs = 352.0 * vv * tot_it / (ms * 1e-3) / 1e9
+        res[f"cg_{label}"] = {"stop": mode, "ms": ms, "iterations_max": int(iters.max().item()),
+                              "iterations_mean": float(iters.double().mean().item()),
+                              "achieved": gbs, "unit": "GB/s", "frac": gbs / hbm_peak,
+                              "bytes_model": "352 B/site/iteration",
+                              "effective": label == "resident"}
+        rel = float(info.relres_dev.max().item())
+        res[f"cg_{label}"]["max_rel_residual"] = rel
+    del q, psi, out, op, x
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    hbm_peak, peak_kind = peaks()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(args.cpu_seconds, args.outer)   # before CUDA init (fork-safe)
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200 import _lib
+    from paper_1512_03812_b200 import fermion as F
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    chains = args.chains
+    cfg = sw.HmcConfig(h=1.0 / args.outer, **CFG3)
+    geom = sw.LatticeGeom(cfg.L, cfg.T)
+    drng = sw.DeviceRng(seed=2024, stream0=rank * chains)
+    q = sw.hot_start(sw.make_rng(2024, rank), geom, batch=chains)
+
+    for _ in range(args.warmup):
+        q, st = sw.hmc_update_ensemble(q, cfg, device_rng=drng)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    F.CG_PROFILE = []
+    launches0 = _lib.launch_count()
+    acc, dhs = [], []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        q, st = sw.hmc_update_ensemble(q, cfg, device_rng=drng)
+        acc.append(st.accepted.mean())
+        dhs.append(np.abs(st.dh).mean())
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    launches = _lib.launch_count() - launches0
+    clk = clocks.stop()
+    prof, F.CG_PROFILE = F.CG_PROFILE, None
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = chains * world / (ms_step * 1e-3)
+
+    # dominant kernel: the resident CG (one launch per solve)
+    cg_ms = sum(a.elapsed_time(b) for a, b, _, _ in prof)
+    cg_iters = sum(int(it.sum().item()) for _, _, it, _ in prof)
+    V = cfg.L * cfg.T
+    n_solves = len(prof)
+    cg_bytes = 352.0 * V * cg_iters
+    cg_flops = 152.0 * V * cg_iters
+    achieved = cg_bytes / (cg_ms * 1e-3) / 1e9
+    fp64_peak = fp64_probe(torch, _lib)
+    solves_per_traj = n_solves / args.steps
+
+    # ensemble observables: one NCCL all-gather at the end (the only collective)
+    acc_rate = float(np.mean(acc))
+    if world > 1:
+        t = torch.tensor([acc_rate, float(np.mean(dhs))], dtype=torch.float64, device="cuda")
+        allv = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allv, t)
+        acc_rate = float(np.mean([v[0].item() for v in allv]))
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        q_host = q.cpu().pin_memory()
+        q_back = torch.empty_like(q_host).pin_memory()
+        h2d = q_host.numel() * 8
+        steps_e2e = max(2, args.steps // 2)
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(steps_e2e):
+            qd = q_host.to("cuda", non_blocking=True)
+            qd, st = sw.hmc_update_ensemble(qd, cfg, device_rng=drng)
+            q_back.copy_(qd, non_blocking=True)
+        f1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        d2h = q_back.numel() * 8 + chains * (8 + 4)
+        e2e = {"value": chains * world / (ems / steps_e2e * 1e-3), "unit": "chain-trajectories/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": ems / steps_e2e}
+
+    stencil = None
+    if rank == 0 and not args.no_stencil:
+        stencil = stencil_bench(torch, sw, _lib, hbm_peak)
+
+    if rank == 0:
+        line = {
+            "metric": "HMC trajectories/s", "value": value, "unit": "chain-trajectories/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64/c128", "data": "synthetic (hot start, device Philox heatbaths)",
+            "config": {"workload": "cfg3: independent 16x16 chains, beta=2.0, m0=0.1, tau=1, "
+                                   f"adapted-nested-fg {args.outer}x2 steps (h={1.0 / args.outer}), "
+                                   "CG tol 1e-10 per-chain stop, complex128",
+                       "chains_per_gpu": chains, "global_chains": chains * world,
+                       "parallelism": f"chain-ensemble dp{world}",
+                       "l2": "working set > L2 (126 MB); no flush needed",
+                       "acceptance": acc_rate, "cg_solves_per_traj": solves_per_traj,
+                       "inversions_per_traj_reference_convention": st.inversions,
+                       "cg_iterations_per_chain_traj": cg_iters / (chains * args.steps)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None,
+                         "peak_kind": peak_kind,
+                         "kernel": "k_cg_resident (per-chain CG, one CTA per chain)",
+                         "bytes_model": "352 B/site/CG-iteration (SURVEY 8(d)), "
+                                        f"{V} sites x {cg_iters} chain-iterations",
+                         "effective": True,
+                         "note": "working set is SMEM/register resident; true bound is FP64 "
+                                 "issue / shared-memory bandwidth",
+                         "fp64_tflops": cg_flops / (cg_ms * 1e-3) / 1e12,
+                         "fp64_peak_tflops_probe": fp64_peak,
+                         "fp64_frac": cg_flops / (cg_ms * 1e-3) / 1e12 / fp64_peak,
+                         "cg_share_of_step": cg_ms / ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+            "stencil": stencil,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

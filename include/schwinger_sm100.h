@@ -147,6 +147,11 @@ int sch_rng_normal(sch_ctx* ctx, double* out, int B, long long per_chain, uint64
 int sch_rng_uniform(sch_ctx* ctx, double* out, int B, long long per_chain, uint64_t seed,
                     uint64_t stream0, uint64_t ctr);
 
+/* ---- measurement probe (bench.py) ------------------------------------ */
+/* FP64 FMA issue-rate probe: blocks x 256 threads x iters x 32 DFMA
+ * (flops = blocks*256*iters*64); scratch needs `blocks` doubles. */
+int sch_probe_fp64(sch_ctx* ctx, double* scratch, int blocks, int iters);
+
 #ifdef __cplusplus
 }
 #endif

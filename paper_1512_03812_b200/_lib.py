@@ -60,6 +60,7 @@ _SIGNATURES = {
     "sch_rng_uniform": [_c_ptr, _c_ptr, _c_int, _c_ll, _c_u64, _c_u64, _c_u64],
     "sch_select_chains": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_int, _c_ll],
     "sch_metropolis": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_int],
+    "sch_probe_fp64": [_c_ptr, _c_ptr, _c_int, _c_int],
 }
 _RESTYPES = {"sch_last_error": ctypes.c_char_p, "sch_launch_count": ctypes.c_ulonglong,
              "sch_build_info": ctypes.c_char_p}

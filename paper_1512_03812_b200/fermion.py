@@ -233,6 +233,12 @@ def spinor_norm(a) -> torch.Tensor:
 # conjugate gradient on the normal equations (fermion.py:171-217)
 # ---------------------------------------------------------------------------
 
+# When set to a list, every cg_solve appends (start_event, end_event,
+# iters_tensor, sites_per_chain) so a benchmark can time the CG kernels on
+# their own stream and count the iterations they ran.
+CG_PROFILE: list | None = None
+
+
 def cg_solve(op: WilsonDirac, b, tol: float, maxiter: int = DEFAULT_MAXITER, x0=None,
              stop: str = "batch_global"):
     """Device-side CG; returns (x, CgInfo) without synchronising."""
@@ -246,9 +252,16 @@ def cg_solve(op: WilsonDirac, b, tol: float, maxiter: int = DEFAULT_MAXITER, x0=
     iters = torch.empty((B,), dtype=torch.int32, device=dev)
     relres = torch.empty((B,), dtype=torch.float64, device=dev)
     status = torch.empty((B,), dtype=torch.int32, device=dev)
+    prof = CG_PROFILE
+    if prof is not None:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
     _lib.ctx().call("sch_cg_normal", _lib.ptr(U), _lib.ptr(b), _lib.ptr(x), _lib.ptr(x0), B, op.L,
                     op.T, op.m0, float(tol), int(maxiter), STOP_MODES[stop], _lib.ptr(iters),
                     _lib.ptr(relres), _lib.ptr(status), None)
+    if prof is not None:
+        ev1.record()
+        prof.append((ev0, ev1, iters, op.L * op.T))
     return x, CgInfo(iters, relres, status, len(bshape) > 0, stop, maxiter)
 
 
