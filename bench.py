@@ -247,12 +247,13 @@ def stencil_bench(torch, sw, _lib, hbm_peak):
     psi = torch.randn((B, L, L, 2), dtype=torch.complex128, device="cuda", generator=gen)
     op = sw.WilsonDirac(q, 0.1)
     out = op.normal(psi)
+    ctx = _lib.ctx()
     torch.cuda.synchronize()
     reps = 20
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(reps):
-        op.normal(psi)
+    for _ in range(reps):   # the C-ABI call itself, output preallocated
+        ctx.call("sch_ddagd", _lib.ptr(op.U), _lib.ptr(psi), _lib.ptr(out), B, L, L, 0.1)
     e1.record()
     torch.cuda.synchronize()
     t = e0.elapsed_time(e1) / reps * 1e-3
@@ -308,6 +309,10 @@ def run_ours(args):
     def barrier():
         if world > 1:
             dist.barrier()
+
+    stencil = None
+    if rank == 0 and not args.no_stencil:   # fresh allocator / caches
+        stencil = stencil_bench(torch, sw, _lib, hbm_peak)
 
     chains = args.chains
     cfg = sw.HmcConfig(h=1.0 / args.outer, **CFG3)
@@ -392,10 +397,6 @@ def run_ours(args):
         e2e = {"value": chains * world / (ems / steps_e2e * 1e-3), "unit": "chain-trajectories/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems / steps_e2e}
-
-    stencil = None
-    if rank == 0 and not args.no_stencil:
-        stencil = stencil_bench(torch, sw, _lib, hbm_peak)
 
     if rank == 0:
         line = {

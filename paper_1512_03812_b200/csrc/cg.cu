@@ -28,253 +28,21 @@
 #include "common.cuh"
 #include "runtime.hpp"
 #include "tile.cuh"
+#include "resident.cuh"
+#include <cstdio>
+#include <cstdlib>
 #include "../../include/schwinger_sm100.h"
 
 namespace {
 
-constexpr int kReplace = 50;   // residual replacement period (fermion.py:199)
+constexpr int kReplace = kResReplace;   // residual replacement period (fermion.py:199)
 
 // ============================================================ resident CG
-struct ResArgs {
-  const double2* __restrict__ U;   // [B][2][V]
-  const double2* __restrict__ b;   // [B][V][2]
-  const double2* __restrict__ x0;  // may be null
-  double2* __restrict__ x;         // out
-  double2* __restrict__ pscr;      // [B][V][2] scratch (rare path)
-  int* __restrict__ iters;
-  double* __restrict__ relres;
-  int* __restrict__ status;
-  int L, T;
-  double diag, tol;
-  int maxiter;
-};
-
-template <int NT, int SPT>
-__global__ void __launch_bounds__(NT) k_cg_resident(ResArgs a) {
-  extern __shared__ double2 sm[];
-  __shared__ double red[3][NT / 32];
-  const int L = a.L, T = a.T, V = L * T;
-  double2* sU0 = sm;
-  double2* sU1 = sm + V;
-  double2* sP0 = sm + 2 * V;
-  double2* sP1 = sm + 3 * V;
-  double2* sT0 = sm + 4 * V;
-  double2* sT1 = sm + 5 * V;
-  const int c = blockIdx.x;
-  const long long cb = (long long)c * V;
-  const int tid = threadIdx.x;
-
-  for (int i = tid; i < 2 * V; i += NT) sm[i] = a.U[2 * cb + i];
-
-  int site[SPT], nxp[SPT], nxm[SPT], ntp[SPT], ntm[SPT];
-  Spinor x[SPT], r[SPT];
-  double bb = 0.0;
-#pragma unroll
-  for (int k = 0; k < SPT; ++k) {
-    int s = tid + k * NT;
-    site[k] = s < V ? s : -1;
-    if (s < V) {
-      int xx = s / T, tt = s - xx * T;
-      nxp[k] = (xx + 1 == L ? 0 : xx + 1) * T + tt;
-      nxm[k] = (xx == 0 ? L - 1 : xx - 1) * T + tt;
-      ntp[k] = xx * T + (tt + 1 == T ? 0 : tt + 1);
-      ntm[k] = xx * T + (tt == 0 ? T - 1 : tt - 1);
-      r[k] = ldg_spinor(a.b, cb + s);
-      bb += spinor_norm2(r[k]);
-    } else {
-      nxp[k] = nxm[k] = ntp[k] = ntm[k] = 0;
-      r[k].s0 = r[k].s1 = make_double2(0, 0);
-    }
-    x[k].s0 = x[k].s1 = make_double2(0, 0);
-  }
-  const double normb2 = block_sum<NT>(bb, red[0]);
-  const double normb = sqrt(normb2);
-  const double target = a.tol * normb;
-  if (normb == 0.0) {   // fermion.py:181-182 (per chain)
-#pragma unroll
-    for (int k = 0; k < SPT; ++k)
-      if (site[k] >= 0) st_spinor(a.x, cb + site[k], x[k]);
-    if (tid == 0) {
-      a.iters[c] = 0;
-      a.relres[c] = 0.0;
-      a.status[c] = 0;
-    }
-    return;
-  }
-
-  // D stage: sT = D sP on my sites; Ddag stage returns D^dag sT on my sites
-  auto stage_d = [&]() {
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      if (site[k] < 0) continue;
-      const int s = site[k];
-      Spinor cc{sP0[s], sP1[s]};
-      Spinor xp{sP0[nxp[k]], sP1[nxp[k]]}, xm{sP0[nxm[k]], sP1[nxm[k]]};
-      Spinor tp{sP0[ntp[k]], sP1[ntp[k]]}, tm{sP0[ntm[k]], sP1[ntm[k]]};
-      Spinor o = wilson_site<false>(cc, xp, xm, tp, tm, sU0[s], sU0[nxm[k]], sU1[s], sU1[ntm[k]],
-                                    a.diag);
-      sT0[s] = o.s0;
-      sT1[s] = o.s1;
-    }
-  };
-  auto stage_ddag = [&](int k) {
-    const int s = site[k];
-    Spinor cc{sT0[s], sT1[s]};
-    Spinor xp{sT0[nxp[k]], sT1[nxp[k]]}, xm{sT0[nxm[k]], sT1[nxm[k]]};
-    Spinor tp{sT0[ntp[k]], sT1[ntp[k]]}, tm{sT0[ntm[k]], sT1[ntm[k]]};
-    return wilson_site<true>(cc, xp, xm, tp, tm, sU0[s], sU0[nxm[k]], sU1[s], sU1[ntm[k]], a.diag);
-  };
-
-  double rs = normb2;   // r = b exactly: same sum as normb^2 (fermion.py:186,191)
-  if (a.x0) {
-#pragma unroll
-    for (int k = 0; k < SPT; ++k)
-      if (site[k] >= 0) {
-        x[k] = ldg_spinor(a.x0, cb + site[k]);
-        sP0[site[k]] = x[k].s0;
-        sP1[site[k]] = x[k].s1;
-      }
-    __syncthreads();
-    stage_d();
-    __syncthreads();
-    double rr = 0.0;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k)
-      if (site[k] >= 0) {
-        Spinor ax = stage_ddag(k);
-        r[k].s0 = csub(r[k].s0, ax.s0);
-        r[k].s1 = csub(r[k].s1, ax.s1);
-        rr += spinor_norm2(r[k]);
-      }
-    rs = block_sum<NT>(rr, red[1]);   // also orders the sP reads before the writes below
-  }
-#pragma unroll
-  for (int k = 0; k < SPT; ++k)
-    if (site[k] >= 0) {
-      sP0[site[k]] = r[k].s0;
-      sP1[site[k]] = r[k].s1;
-    }
-
-  double best = INFINITY;
-  for (int it = 1; it <= a.maxiter; ++it) {
-    __syncthreads();
-    stage_d();
-    __syncthreads();
-    Spinor ap[SPT];
-    double pap = 0.0;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      if (site[k] < 0) continue;
-      ap[k] = stage_ddag(k);
-      Spinor pk{sP0[site[k]], sP1[site[k]]};
-      pap += spinor_redot(pk, ap[k]);
-    }
-    const double den = block_sum<NT>(pap, red[0]);
-    const double alpha = den > 0.0 ? rs / den : 0.0;
-    const bool repl = (it % kReplace) == 0;
-    double rsn = 0.0;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      if (site[k] < 0) continue;
-      const int s = site[k];
-      double2 p0 = sP0[s], p1 = sP1[s];
-      x[k].s0 = make_double2(__fma_rn(alpha, p0.x, x[k].s0.x), __fma_rn(alpha, p0.y, x[k].s0.y));
-      x[k].s1 = make_double2(__fma_rn(alpha, p1.x, x[k].s1.x), __fma_rn(alpha, p1.y, x[k].s1.y));
-      if (!repl) {
-        r[k].s0 = make_double2(__fma_rn(-alpha, ap[k].s0.x, r[k].s0.x),
-                               __fma_rn(-alpha, ap[k].s0.y, r[k].s0.y));
-        r[k].s1 = make_double2(__fma_rn(-alpha, ap[k].s1.x, r[k].s1.x),
-                               __fma_rn(-alpha, ap[k].s1.y, r[k].s1.y));
-        rsn += spinor_norm2(r[k]);
-      }
-    }
-    double rs_new = 0.0;
-    bool check = true;
-    if (!repl) {
-      rs_new = block_sum<NT>(rsn, red[1]);
-      check = sqrt(rs_new) <= target;
-    }
-    bool from_scratch = false;
-    if (check) {
-      // true residual b - A x (residual replacement shares this path)
-#pragma unroll
-      for (int k = 0; k < SPT; ++k)
-        if (site[k] >= 0) {
-          a.pscr[2 * (cb + site[k])] = sP0[site[k]];
-          a.pscr[2 * (cb + site[k]) + 1] = sP1[site[k]];
-        }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < SPT; ++k)
-        if (site[k] >= 0) {
-          sP0[site[k]] = x[k].s0;
-          sP1[site[k]] = x[k].s1;
-        }
-      __syncthreads();
-      stage_d();
-      __syncthreads();
-      double tn2 = 0.0;
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) {
-        if (site[k] < 0) continue;
-        Spinor ax = stage_ddag(k);
-        Spinor bk = ldg_spinor(a.b, cb + site[k]);
-        ap[k].s0 = csub(bk.s0, ax.s0);
-        ap[k].s1 = csub(bk.s1, ax.s1);
-        tn2 += spinor_norm2(ap[k]);
-      }
-      tn2 = block_sum<NT>(tn2, red[2]);
-      const double tn = sqrt(tn2);
-      if (!repl || tn <= target) best = tn / normb;
-      if (tn <= target) {
-#pragma unroll
-        for (int k = 0; k < SPT; ++k)
-          if (site[k] >= 0) st_spinor(a.x, cb + site[k], x[k]);
-        if (tid == 0) {
-          a.iters[c] = it;
-          a.relres[c] = tn / normb;
-          a.status[c] = 0;
-        }
-        return;
-      }
-#pragma unroll
-      for (int k = 0; k < SPT; ++k)
-        if (site[k] >= 0) r[k] = ap[k];
-      rs_new = tn2;
-      from_scratch = true;
-    }
-    const double beta = rs > 0.0 ? rs_new / rs : 0.0;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      if (site[k] < 0) continue;
-      const int s = site[k];
-      double2 p0, p1;
-      if (from_scratch) {
-        p0 = a.pscr[2 * (cb + s)];
-        p1 = a.pscr[2 * (cb + s) + 1];
-      } else {
-        p0 = sP0[s];
-        p1 = sP1[s];
-      }
-      sP0[s] = make_double2(__fma_rn(beta, p0.x, r[k].s0.x), __fma_rn(beta, p0.y, r[k].s0.y));
-      sP1[s] = make_double2(__fma_rn(beta, p1.x, r[k].s1.x), __fma_rn(beta, p1.y, r[k].s1.y));
-    }
-    rs = rs_new;
-  }
-  // iteration cap (fermion.py:216-217)
-#pragma unroll
-  for (int k = 0; k < SPT; ++k)
-    if (site[k] >= 0) st_spinor(a.x, cb + site[k], x[k]);
-  if (tid == 0) {
-    a.iters[c] = a.maxiter;
-    a.relres[c] = fmin(best, sqrt(rs) / normb);
-    a.status[c] = 1;
-  }
-}
+// (kernel in resident.cuh)
 
 template <int NT, int SPT>
 int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
-  const size_t smem = sizeof(double2) * 6 * (size_t)a.L * a.T;
+  const size_t smem = sizeof(double2) * 8 * (size_t)a.L * a.T;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_cg_resident<NT, SPT>,
@@ -285,6 +53,34 @@ int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
   k_cg_resident<NT, SPT><<<B, NT, smem, ctx->stream>>>(a);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
+}
+
+// Threads x sites-per-thread of the resident engine for V sites.  The
+// SCH_RESIDENT environment variable ("NTxSPT", e.g. "128x2") overrides the
+// default for tuning runs.
+int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
+  static int forced_nt = -1, forced_spt = -1;
+  if (forced_nt < 0) {
+    forced_nt = forced_spt = 0;
+    if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%d", &forced_nt, &forced_spt);
+  }
+  int nt = 0, spt = 0;
+  if (forced_nt > 0 && (long long)forced_nt * forced_spt >= V) {
+    nt = forced_nt;
+    spt = forced_spt;
+  } else if (V <= 128) { nt = 128; spt = 1; }
+  else if (V <= 256) { nt = 128; spt = 2; }
+  else if (V <= 512) { nt = 256; spt = 2; }
+  else { nt = 256; spt = 4; }
+  if (nt == 128 && spt == 1) return launch_resident<128, 1>(ctx, a, B);
+  if (nt == 128 && spt == 2) return launch_resident<128, 2>(ctx, a, B);
+  if (nt == 256 && spt == 1) return launch_resident<256, 1>(ctx, a, B);
+  if (nt == 256 && spt == 2) return launch_resident<256, 2>(ctx, a, B);
+  if (nt == 256 && spt == 4) return launch_resident<256, 4>(ctx, a, B);
+  if (nt == 512 && spt == 1) return launch_resident<512, 1>(ctx, a, B);
+  if (nt == 512 && spt == 2) return launch_resident<512, 2>(ctx, a, B);
+  if (nt == 1024 && spt == 1) return launch_resident<1024, 1>(ctx, a, B);
+  return sch_fail(ctx, SCH_ERR_ARG, "no resident CG instantiation %dx%d", nt, spt);
 }
 
 // =========================================================== streaming CG
@@ -335,14 +131,14 @@ __global__ void k_cg_init(ElemArgs e, StreamState st) {
   for (int k = threadIdx.x; k < e.TX * e.TT; k += blockDim.x) {
     long long s;
     if (!tile_site(e, tile, k, s)) continue;
-    Spinor bv = ldg_spinor(e.b, cb + s);
+    Spinor bv = ld256_spinor_nc(e.b, cb + s);
     acc += spinor_norm2(bv);
     Spinor xv;
-    if (e.x0) xv = ldg_spinor(e.x0, cb + s);
+    if (e.x0) xv = ld256_spinor_nc(e.x0, cb + s);
     else xv.s0 = xv.s1 = make_double2(0, 0);
-    st_spinor(e.x, cb + s, xv);
-    st_spinor(e.r, cb + s, bv);
-    st_spinor(e.p, cb + s, bv);
+    st256_spinor(e.x, cb + s, xv);
+    st256_spinor(e.r, cb + s, bv);
+    st256_spinor(e.p, cb + s, bv);
   }
   double s = block_sum_rt(acc, slot);
   if (threadIdx.x == 0) st.part_bb[blockIdx.x] = s;
@@ -355,7 +151,7 @@ __global__ void k_copy_r_to_p(ElemArgs e) {
   for (int k = threadIdx.x; k < e.TX * e.TT; k += blockDim.x) {
     long long s;
     if (!tile_site(e, tile, k, s)) continue;
-    st_spinor(e.p, cb + s, ld_spinor(e.r, cb + s));
+    st256_spinor(e.p, cb + s, ld256_spinor(e.r, cb + s));
   }
 }
 
@@ -370,20 +166,16 @@ __global__ void k_cg_update(ElemArgs e, StreamState st, int repl) {
   for (int k = threadIdx.x; k < e.TX * e.TT; k += blockDim.x) {
     long long s;
     if (!tile_site(e, tile, k, s)) continue;
-    const long long o = 2 * (cb + s);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      double2 rv = e.r[o + h], pv = e.p[o + h], xv = e.x[o + h];
-      pv = make_double2(__fma_rn(be, pv.x, rv.x), __fma_rn(be, pv.y, rv.y));
-      xv = make_double2(__fma_rn(al, pv.x, xv.x), __fma_rn(al, pv.y, xv.y));
-      e.p[o + h] = pv;
-      e.x[o + h] = xv;
-      if (!repl) {
-        double2 av = __ldg(e.ap + o + h);
-        rv = make_double2(__fma_rn(-al, av.x, rv.x), __fma_rn(-al, av.y, rv.y));
-        e.r[o + h] = rv;
-        acc += rv.x * rv.x + rv.y * rv.y;
-      }
+    Spinor rv = ld256_spinor(e.r, cb + s), pv = ld256_spinor(e.p, cb + s);
+    Spinor xv = ld256_spinor(e.x, cb + s);
+    pv = sp_fma(be, pv, rv);
+    xv = sp_fma(al, pv, xv);
+    st256_spinor(e.p, cb + s, pv);
+    st256_spinor(e.x, cb + s, xv);
+    if (!repl) {
+      rv = sp_fma(-al, ld256_spinor_nc(e.ap, cb + s), rv);
+      st256_spinor(e.r, cb + s, rv);
+      acc += spinor_norm2(rv);
     }
   }
   if (!repl) {
@@ -734,17 +526,10 @@ extern "C" int sch_cg_normal(sch_ctx* ctx, const double* U, const double* b, dou
   const long long V = (long long)L * T;
   const bool per_chain = stop_mode == 1 || B == 1;
   int rc = SCH_OK;
-  if (per_chain && V <= 2048) {
-    void* ws;
-    rc = sch_workspace(ctx, sizeof(double2) * 2 * (size_t)B * V, &ws);
-    if (rc) return rc;
-    ResArgs a{(const double2*)U, (const double2*)b, (const double2*)x0, (double2*)x, (double2*)ws,
-              iters, relres, status, L, T, 2.0 + m0, tol, maxiter};
-    if (V <= 128) rc = launch_resident<128, 1>(ctx, a, B);
-    else if (V <= 256) rc = launch_resident<128, 2>(ctx, a, B);
-    else if (V <= 512) rc = launch_resident<256, 2>(ctx, a, B);
-    else if (V <= 1024) rc = launch_resident<256, 4>(ctx, a, B);
-    else rc = launch_resident<512, 4>(ctx, a, B);
+  if (per_chain && V <= 1024) {
+    ResArgs a{(const double2*)U, (const double2*)b, (const double2*)x0, (double2*)x, iters, relres,
+              status, L, T, 2.0 + m0, tol, maxiter};
+    rc = resident_dispatch(ctx, a, B, V);
   } else {
     rc = cg_streaming(ctx, (const double2*)U, (const double2*)b, (double2*)x, (const double2*)x0, B,
                       L, T, m0, tol, maxiter, per_chain ? 0 : 1, iters, relres, status);

@@ -96,6 +96,29 @@ SCH_DEV void st_spinor(double2* __restrict__ p, long site, const Spinor& v) {
   p[2 * site] = v.s0;
   p[2 * site + 1] = v.s1;
 }
+// One 256-bit access per site (sm_100a LDG/STG.E.ENL2.256): a warp moves
+// 1 KiB of spinors per instruction, fully coalesced, no half-used sectors.
+// `p` must be 32-B aligned at the site (true for every [..][V][2] c128 field).
+SCH_DEV Spinor ld256_spinor_nc(const double2* __restrict__ p, long long site) {
+  Spinor v;
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v.s0.x), "=d"(v.s0.y), "=d"(v.s1.x), "=d"(v.s1.y)
+               : "l"(p + 2 * site));
+  return v;
+}
+SCH_DEV Spinor ld256_spinor(const double2* p, long long site) {
+  Spinor v;
+  asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v.s0.x), "=d"(v.s0.y), "=d"(v.s1.x), "=d"(v.s1.y)
+               : "l"(p + 2 * site));
+  return v;
+}
+SCH_DEV void st256_spinor(double2* p, long long site, const Spinor& v) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p + 2 * site), "d"(v.s0.x),
+               "d"(v.s0.y), "d"(v.s1.x), "d"(v.s1.y)
+               : "memory");
+}
+
 SCH_DEV double spinor_norm2(const Spinor& v) {
   return v.s0.x * v.s0.x + v.s0.y * v.s0.y + v.s1.x * v.s1.x + v.s1.y * v.s1.y;
 }

@@ -69,14 +69,14 @@ __global__ void __launch_bounds__(NT) k_normal_tile(TileArgs a) {
   for (int k = threadIdx.x; k < NR; k += NT) {
     const int i = k / RT, j = k - (k / RT) * RT;
     const long long site = cbase + (long long)gx[i] * T + gt[j];
-    double2 v0 = __ldg(a.in + 2 * site), v1 = __ldg(a.in + 2 * site + 1);
+    Spinor v = ld256_spinor_nc(a.in, site);
     if (MODE == MODE_P) {
-      double2 p0 = __ldg(a.in2 + 2 * site), p1 = __ldg(a.in2 + 2 * site + 1);
-      v0 = make_double2(__fma_rn(beta_c, p0.x, v0.x), __fma_rn(beta_c, p0.y, v0.y));
-      v1 = make_double2(__fma_rn(beta_c, p1.x, v1.x), __fma_rn(beta_c, p1.y, v1.y));
+      Spinor p = ld256_spinor_nc(a.in2, site);
+      v.s0 = make_double2(__fma_rn(beta_c, p.s0.x, v.s0.x), __fma_rn(beta_c, p.s0.y, v.s0.y));
+      v.s1 = make_double2(__fma_rn(beta_c, p.s1.x, v.s1.x), __fma_rn(beta_c, p.s1.y, v.s1.y));
     }
-    sA[0][k] = v0;
-    sA[1][k] = v1;
+    sA[0][k] = v.s0;
+    sA[1][k] = v.s1;
   }
   __syncthreads();
 
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(NT) k_normal_tile(TileArgs a) {
     Spinor r = wilson_site<true>(cc, xp, xm, tp, tm, u0, u0m, u1, u1m, a.diag);
     const long long site = cbase + (long long)X * T + Tt;
     if (MODE == MODE_X) {
-      Spinor bb = ldg_spinor(a.bvec, site);
+      Spinor bb = ld256_spinor_nc(a.bvec, site);
       r.s0 = csub(bb.s0, r.s0);
       r.s1 = csub(bb.s1, r.s1);
       part += spinor_norm2(r);
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(NT) k_normal_tile(TileArgs a) {
       Spinor pp{sA[0][i * RT + j], sA[1][i * RT + j]};
       part += spinor_redot(pp, r);
     }
-    st_spinor(a.out, site, r);
+    st256_spinor(a.out, site, r);
   }
   if (MODE != MODE_PLAIN) {
     double s = block_sum<NT>(part, slot);

@@ -55,14 +55,14 @@ __global__ void k_dslash(const double2* __restrict__ U, long long ustride,
     int tp = t + 1 == g.T ? 0 : t + 1, tm = t == 0 ? g.T - 1 : t - 1;
     long long cb = b * g.V;
     const double2* Uc = U + b * ustride;
-    Spinor c = ldg_spinor(psi, cb + s);
-    Spinor vxp = ldg_spinor(psi, cb + xp * g.T + t);
-    Spinor vxm = ldg_spinor(psi, cb + xm * g.T + t);
-    Spinor vtp = ldg_spinor(psi, cb + x * g.T + tp);
-    Spinor vtm = ldg_spinor(psi, cb + x * g.T + tm);
+    Spinor c = ld256_spinor_nc(psi, cb + s);
+    Spinor vxp = ld256_spinor_nc(psi, cb + xp * g.T + t);
+    Spinor vxm = ld256_spinor_nc(psi, cb + xm * g.T + t);
+    Spinor vtp = ld256_spinor_nc(psi, cb + x * g.T + tp);
+    Spinor vtm = ld256_spinor_nc(psi, cb + x * g.T + tm);
     double2 u0 = __ldg(Uc + s), u1 = __ldg(Uc + g.V + s);
     double2 u0m = __ldg(Uc + xm * g.T + t), u1m = __ldg(Uc + g.V + x * g.T + tm);
-    st_spinor(out, cb + s, wilson_site<DAG>(c, vxp, vxm, vtp, vtm, u0, u0m, u1, u1m, diag));
+    st256_spinor(out, cb + s, wilson_site<DAG>(c, vxp, vxm, vtp, vtm, u0, u0m, u1, u1m, diag));
   }
 }
 
@@ -135,9 +135,9 @@ __global__ void k_fermion_force(const double2* __restrict__ U, const double2* __
     int x = s / g.T, t = s - x * g.T;
     int xp = x + 1 == g.L ? 0 : x + 1, tp = t + 1 == g.T ? 0 : t + 1;
     long long cb = b * g.V;
-    Spinor cn = ldg_spinor(chi, cb + s), xn = ldg_spinor(xi, cb + s);
-    Spinor cx = ldg_spinor(chi, cb + xp * g.T + t), xx = ldg_spinor(xi, cb + xp * g.T + t);
-    Spinor ct = ldg_spinor(chi, cb + x * g.T + tp), xt = ldg_spinor(xi, cb + x * g.T + tp);
+    Spinor cn = ld256_spinor_nc(chi, cb + s), xn = ld256_spinor_nc(xi, cb + s);
+    Spinor cx = ld256_spinor_nc(chi, cb + xp * g.T + t), xx = ld256_spinor_nc(xi, cb + xp * g.T + t);
+    Spinor ct = ld256_spinor_nc(chi, cb + x * g.T + tp), xt = ld256_spinor_nc(xi, cb + x * g.T + tp);
     const double2* Uc = U + 2 * cb;
     Bil b0 = bilinear<0>(cn, cx, xn, xx, __ldg(Uc + s));
     Bil b1 = bilinear<1>(cn, ct, xn, xt, __ldg(Uc + g.V + s));
@@ -187,8 +187,8 @@ __global__ void k_wsums(const double2* __restrict__ U, const double* __restrict_
         sf = x * g.T + (t + 1 == g.T ? 0 : t + 1);
         sb = x * g.T + (t == 0 ? g.T - 1 : t - 1);
       }
-      Spinor cb_ = ldg_spinor(chi, cb + sb), cf = ldg_spinor(chi, cb + sf);
-      Spinor xb = ldg_spinor(xi, cb + sb), xf = ldg_spinor(xi, cb + sf);
+      Spinor cb_ = ld256_spinor_nc(chi, cb + sb), cf = ld256_spinor_nc(chi, cb + sf);
+      Spinor xb = ld256_spinor_nc(xi, cb + sb), xf = ld256_spinor_nc(xi, cb + sf);
       double2 un = __ldg(Uc + nu * g.V + s), ub = __ldg(Uc + nu * g.V + sb);
       double wn = __ldg(Wc + nu * g.V + s), wb = __ldg(Wc + nu * g.V + sb);
       double2 wm_cb = nu == 0 ? wminus0(cb_) : wminus1(cb_);
@@ -238,10 +238,10 @@ __global__ void k_fg_combine(const double2* __restrict__ U, const double2* __res
 #pragma unroll
     for (int mu = 0; mu < 2; ++mu) {
       int sf = mu == 0 ? (x + 1 == g.L ? 0 : x + 1) * g.T + t : x * g.T + (t + 1 == g.T ? 0 : t + 1);
-      Spinor z1n = ldg_spinor(z1, cb + s), z1f = ldg_spinor(z1, cb + sf);
-      Spinor z2n = ldg_spinor(z2, cb + s), z2f = ldg_spinor(z2, cb + sf);
-      Spinor cn = ldg_spinor(chi, cb + s), cf = ldg_spinor(chi, cb + sf);
-      Spinor xn = ldg_spinor(xi, cb + s), xf = ldg_spinor(xi, cb + sf);
+      Spinor z1n = ld256_spinor_nc(z1, cb + s), z1f = ld256_spinor_nc(z1, cb + sf);
+      Spinor z2n = ld256_spinor_nc(z2, cb + s), z2f = ld256_spinor_nc(z2, cb + sf);
+      Spinor cn = ld256_spinor_nc(chi, cb + s), cf = ld256_spinor_nc(chi, cb + sf);
+      Spinor xn = ld256_spinor_nc(xi, cb + s), xf = ld256_spinor_nc(xi, cb + sf);
       double2 u = __ldg(Uc + mu * g.V + s);
       Bil a1 = mu == 0 ? bilinear<0>(z1n, z1f, xn, xf, u) : bilinear<1>(z1n, z1f, xn, xf, u);
       Bil a2 = mu == 0 ? bilinear<0>(cn, cf, z2n, z2f, u) : bilinear<1>(cn, cf, z2n, z2f, u);
