@@ -156,11 +156,22 @@ __global__ void k_copy_r_to_p(ElemArgs e) {
 }
 
 // update: p = r + beta p; x += alpha p; (non-replacement) r -= alpha ap, partial ||r||^2
+// With few tiles per chain (FUSE_ALPHA) every thread forms alpha itself from
+// the chain's <p,Ap> tile partials, in the same fixed order as k_ctrl_alpha.
+template <bool FUSE_ALPHA>
 __global__ void k_cg_update(ElemArgs e, StreamState st, int repl) {
   __shared__ double slot[32];
   const int c = blockIdx.x / e.tpc, tile = blockIdx.x - c * e.tpc;
   if (!st.active[c]) return;
-  const double al = st.alpha[c], be = st.beta[c];
+  double al;
+  if (FUSE_ALPHA) {
+    double den = 0.0;
+    for (int k = 0; k < e.tpc; ++k) den += st.part_pap[(long long)c * e.tpc + k];
+    al = den > 0.0 ? st.rs[c] / den : 0.0;
+  } else {
+    al = st.alpha[c];
+  }
+  const double be = st.beta[c];
   const long long cb = (long long)c * e.L * e.T;
   double acc = 0.0;
   for (int k = threadIdx.x; k < e.TX * e.TT; k += blockDim.x) {
@@ -184,19 +195,42 @@ __global__ void k_cg_update(ElemArgs e, StreamState st, int repl) {
   }
 }
 
+// Per-chain sum of tile partials in a fixed order.  Control kernels run in
+// one of two layouts: one thread per chain (few tiles per chain, sequential
+// sum) or one CTA per chain (many tiles, tree sum).
+constexpr int kSmallTpc = 16;
+
+template <bool PER_THREAD>
+__device__ __forceinline__ int ctrl_chain() {
+  return PER_THREAD ? (int)(blockIdx.x * blockDim.x + threadIdx.x) : (int)blockIdx.x;
+}
+
+template <bool PER_THREAD>
+__device__ __forceinline__ bool ctrl_leader() {
+  return PER_THREAD ? true : threadIdx.x == 0;
+}
+
+template <bool PER_THREAD>
 __device__ __forceinline__ double sum_partials(const double* part, int tpc, int c, double* slot) {
+  if (PER_THREAD) {
+    double acc = 0.0;
+    for (int k = 0; k < tpc; ++k) acc += part[(long long)c * tpc + k];
+    return acc;
+  }
   double acc = 0.0;
   for (int k = threadIdx.x; k < tpc; k += blockDim.x) acc += part[(long long)c * tpc + k];
   return block_sum_rt(acc, slot);
 }
 
 // init control: normb, target, rs, flags
+template <bool PT>
 __global__ void k_ctrl_init(StreamState st, int have_x0) {
   __shared__ double slot[2][32];
-  const int c = blockIdx.x;
-  double nb2 = sum_partials(st.part_bb, st.tpc, c, slot[0]);
-  double rr = have_x0 ? sum_partials(st.part_rr2, st.tpc, c, slot[1]) : nb2;
-  if (threadIdx.x == 0) {
+  const int c = ctrl_chain<PT>();
+  if (c >= st.B) return;
+  double nb2 = sum_partials<PT>(st.part_bb, st.tpc, c, slot[0]);
+  double rr = have_x0 ? sum_partials<PT>(st.part_rr2, st.tpc, c, slot[1]) : nb2;
+  if (ctrl_leader<PT>()) {
     double nb = sqrt(nb2);
     st.normb[c] = nb;
     st.target[c] = st.tol * nb;
@@ -236,28 +270,30 @@ __global__ void k_ctrl_init_global(StreamState st) {
 }
 
 // after the stencil pass: alpha = <p,Ap> > 0 ? rs/<p,Ap> : 0
+template <bool PT>
 __global__ void k_ctrl_alpha(StreamState st) {
   __shared__ double slot[32];
-  const int c = blockIdx.x;
-  if (!st.active[c]) return;
-  double den = sum_partials(st.part_pap, st.tpc, c, slot);
-  if (threadIdx.x == 0) st.alpha[c] = den > 0.0 ? st.rs[c] / den : 0.0;
+  const int c = ctrl_chain<PT>();
+  if (c >= st.B || !st.active[c]) return;
+  double den = sum_partials<PT>(st.part_pap, st.tpc, c, slot);
+  if (ctrl_leader<PT>()) st.alpha[c] = den > 0.0 ? st.rs[c] / den : 0.0;
 }
 
 // after the update: rs' and the convergence check
+template <bool PT>
 __global__ void k_ctrl_check(StreamState st, int repl) {
   __shared__ double slot[32];
-  const int c = blockIdx.x;
-  if (!st.active[c]) return;
+  const int c = ctrl_chain<PT>();
+  if (c >= st.B || !st.active[c]) return;
   if (repl) {
-    if (threadIdx.x == 0) {
+    if (ctrl_leader<PT>()) {
       st.pass[c] = 1;
       st.need_x[c] = 1;
     }
     return;
   }
-  double rsn = sum_partials(st.part_rr, st.tpc, c, slot);
-  if (threadIdx.x == 0) {
+  double rsn = sum_partials<PT>(st.part_rr, st.tpc, c, slot);
+  if (ctrl_leader<PT>()) {
     st.rs_new[c] = rsn;
     int ok = sqrt(rsn) <= st.target[c];
     st.pass[c] = ok;
@@ -280,13 +316,14 @@ __global__ void k_ctrl_check_global(StreamState st, int repl) {
 }
 
 // after the (optional) true-residual pass
+template <bool PT>
 __global__ void k_ctrl_final(StreamState st, int it) {
   __shared__ double slot[32];
-  const int c = blockIdx.x;
-  if (!st.active[c]) return;
+  const int c = ctrl_chain<PT>();
+  if (c >= st.B || !st.active[c]) return;
   const int nx = st.need_x[c];
-  double tn2 = nx ? sum_partials(st.part_rr2, st.tpc, c, slot) : 0.0;
-  if (threadIdx.x != 0) return;
+  double tn2 = nx ? sum_partials<PT>(st.part_rr2, st.tpc, c, slot) : 0.0;
+  if (!ctrl_leader<PT>()) return;
   double rs_new = nx ? tn2 : st.rs_new[c];
   st.rs_new[c] = rs_new;
   if (st.global_mode) return;   // decisions in k_ctrl_final_global
@@ -457,7 +494,12 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
     k_copy_r_to_p<<<ngrid, 256, 0, s>>>(e);
     SCH_LAUNCHED(ctx);
   }
-  k_ctrl_init<<<B, 128, 0, s>>>(st, x0 != nullptr);
+  // control-kernel layout: one thread per chain when chains have few tiles
+  const bool pt = tpc <= kSmallTpc;
+  const unsigned cgrid = pt ? blocks_for(B, 128) : (unsigned)B;
+  const int sparse = ctx->num_sms * 2;   // persistent grid of the true-residual pass
+  if (pt) k_ctrl_init<true><<<cgrid, 128, 0, s>>>(st, x0 != nullptr);
+  else k_ctrl_init<false><<<cgrid, 128, 0, s>>>(st, x0 != nullptr);
   SCH_LAUNCHED(ctx);
   k_ctrl_init_global<<<1, 1024, 0, s>>>(st);
   SCH_LAUNCHED(ctx);
@@ -484,19 +526,27 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
       const int repl = (it % kReplace) == 0;
       launch_normal_tile<MODE_P>(sh, tp, s);
       SCH_LAUNCHED(ctx);
-      k_ctrl_alpha<<<B, 128, 0, s>>>(st);
-      SCH_LAUNCHED(ctx);
-      k_cg_update<<<ngrid, 256, 0, s>>>(e, st, repl);
-      SCH_LAUNCHED(ctx);
-      k_ctrl_check<<<B, 128, 0, s>>>(st, repl);
-      SCH_LAUNCHED(ctx);
+      if (pt) {
+        k_cg_update<true><<<ngrid, 256, 0, s>>>(e, st, repl);
+        SCH_LAUNCHED(ctx);
+        k_ctrl_check<true><<<cgrid, 128, 0, s>>>(st, repl);
+        SCH_LAUNCHED(ctx);
+      } else {
+        k_ctrl_alpha<false><<<cgrid, 128, 0, s>>>(st);
+        SCH_LAUNCHED(ctx);
+        k_cg_update<false><<<ngrid, 256, 0, s>>>(e, st, repl);
+        SCH_LAUNCHED(ctx);
+        k_ctrl_check<false><<<cgrid, 128, 0, s>>>(st, repl);
+        SCH_LAUNCHED(ctx);
+      }
       if (global_mode) {
         k_ctrl_check_global<<<1, 1024, 0, s>>>(st, repl);
         SCH_LAUNCHED(ctx);
       }
-      launch_normal_tile<MODE_X>(sh, txx, s);
+      launch_normal_tile<MODE_X>(sh, txx, s, sparse);
       SCH_LAUNCHED(ctx);
-      k_ctrl_final<<<B, 128, 0, s>>>(st, it);
+      if (pt) k_ctrl_final<true><<<cgrid, 128, 0, s>>>(st, it);
+      else k_ctrl_final<false><<<cgrid, 128, 0, s>>>(st, it);
       SCH_LAUNCHED(ctx);
       if (global_mode) {
         k_ctrl_final_global<<<1, 1024, 0, s>>>(st, it);

@@ -1,10 +1,18 @@
 // Fused D^dag D shared-memory tile kernel (fermion.py:129-131).
 //
-// One CTA computes D^dag D on a TX x TT tile of one chain.  It stages the
-// input spinor on the tile plus a 2-site halo (HX/HT = 2) in shared memory,
-// computes D on the tile plus a 1-site halo into a second shared buffer, then
-// D^dag on the tile.  A direction whose tile spans the whole lattice extent
-// (HX or HT = 0) wraps periodically inside shared memory instead.
+// One CTA computes D^dag D on a TX x TT tile of one chain.  The input spinor
+// is read once per cell of the tile plus a 2-site halo (HX/HT = 2); a
+// direction whose tile spans the whole lattice extent (HX or HT = 0) wraps
+// periodically inside shared memory instead.  Every cell is owned by one
+// thread, which keeps the cell's spinor and its two links in registers and
+// exports the four rank-1 projections its neighbours need (half-spinor
+// exchange, see resident.cuh) — so links are read once, by their owner, and
+// shared-memory traffic is 64 B stored + 64 B loaded per cell per D.
+//
+//   phase A : owner loads psi (256-bit), U_0, U_1; exports D-projections
+//   phase B : D on the tile + 1-site halo (from the exports); re-exports the
+//             D^dag-projections of t = D psi into the same buffer
+//   phase C : D^dag on the tile, epilogue per MODE
 //
 // Compulsory HBM traffic per site: spinor in 32 B + U 32 B + out 32 B = 96 B
 // (SURVEY §8(d)); halo re-reads hit L2.
@@ -18,6 +26,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "resident.cuh"
 
 enum { MODE_PLAIN = 0, MODE_P = 1, MODE_X = 2 };
 
@@ -36,16 +45,10 @@ struct TileArgs {
 };
 
 template <int TX, int TT, int HX, int HT, int MODE, int NT>
-__global__ void __launch_bounds__(NT) k_normal_tile(TileArgs a) {
+__device__ __forceinline__ void tile_body(const TileArgs& a, int c, int tile, double2* E, int* gx,
+                                          int* gxm, int* gt, int* gtm, double* slot) {
   constexpr int RX = TX + 2 * HX, RT = TT + 2 * HT, NR = RX * RT;
-  __shared__ double2 sA[2][NR];
-  __shared__ double2 sD[2][NR];
-  __shared__ int gx[RX], gxm[RX], gt[RT], gtm[RT];
-  __shared__ double slot[NT / 32];
-
-  const int c = blockIdx.x / a.tiles_per_chain;
-  const int tile = blockIdx.x - c * a.tiles_per_chain;
-  if (MODE != MODE_PLAIN && a.flag && a.flag[c] == 0) return;
+  constexpr int CPT = (NR + NT - 1) / NT;   // region cells per thread
   const int tx = tile / a.tiles_t, tt = tile - tx * a.tiles_t;
   const int x0 = tx * TX, t0 = tt * TT;
   const int L = a.L, T = a.T;
@@ -64,84 +67,138 @@ __global__ void __launch_bounds__(NT) k_normal_tile(TileArgs a) {
   }
   __syncthreads();
 
+  const double2* __restrict__ Uc = a.U + 2 * cbase;   // [2][V] of this chain
   double beta_c = 0.0;
   if (MODE == MODE_P) beta_c = a.beta[c];
-  for (int k = threadIdx.x; k < NR; k += NT) {
-    const int i = k / RT, j = k - (k / RT) * RT;
-    const long long site = cbase + (long long)gx[i] * T + gt[j];
-    Spinor v = ld256_spinor_nc(a.in, site);
+
+  // ---- phase A: owner loads; exports D projections
+  Spinor v[CPT], t[CPT];
+  double2 u0[CPT], u1[CPT];
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int k = threadIdx.x + j * NT;
+    if (k >= NR) continue;
+    const int ri = k / RT, rj = k - (k / RT) * RT;
+    const long long s = (long long)gx[ri] * T + gt[rj];
+    v[j] = ld256_spinor_nc(a.in, cbase + s);
     if (MODE == MODE_P) {
-      Spinor p = ld256_spinor_nc(a.in2, site);
-      v.s0 = make_double2(__fma_rn(beta_c, p.s0.x, v.s0.x), __fma_rn(beta_c, p.s0.y, v.s0.y));
-      v.s1 = make_double2(__fma_rn(beta_c, p.s1.x, v.s1.x), __fma_rn(beta_c, p.s1.y, v.s1.y));
+      Spinor p = ld256_spinor_nc(a.in2, cbase + s);
+      v[j].s0 = make_double2(__fma_rn(beta_c, p.s0.x, v[j].s0.x), __fma_rn(beta_c, p.s0.y, v[j].s0.y));
+      v[j].s1 = make_double2(__fma_rn(beta_c, p.s1.x, v[j].s1.x), __fma_rn(beta_c, p.s1.y, v[j].s1.y));
     }
-    sA[0][k] = v.s0;
-    sA[1][k] = v.s1;
+    u0[j] = __ldg(Uc + s);
+    u1[j] = __ldg(Uc + V + s);
+    res_produce<false>(E, NR, k, v[j], u0[j], u1[j]);
   }
   __syncthreads();
 
-  const double2* __restrict__ Uc = a.U + 2 * cbase;   // [2][V] of this chain
-  // ---- stage 1: D on tile + 1-site halo
-  constexpr int DX0 = HX / 2, DXN = RX - 2 * DX0;
-  constexpr int DT0 = HT / 2, DTN = RT - 2 * DT0;
-  for (int k = threadIdx.x; k < DXN * DTN; k += NT) {
-    const int i = DX0 + k / DTN, j = DT0 + (k - (k / DTN) * DTN);
-    const int ip = HX ? i + 1 : (i + 1 == RX ? 0 : i + 1);
-    const int im = HX ? i - 1 : (i == 0 ? RX - 1 : i - 1);
-    const int jp = HT ? j + 1 : (j + 1 == RT ? 0 : j + 1);
-    const int jm = HT ? j - 1 : (j == 0 ? RT - 1 : j - 1);
-    Spinor cc{sA[0][i * RT + j], sA[1][i * RT + j]};
-    Spinor xp{sA[0][ip * RT + j], sA[1][ip * RT + j]};
-    Spinor xm{sA[0][im * RT + j], sA[1][im * RT + j]};
-    Spinor tp{sA[0][i * RT + jp], sA[1][i * RT + jp]};
-    Spinor tm{sA[0][i * RT + jm], sA[1][i * RT + jm]};
-    const int X = gx[i], Tt = gt[j];
-    double2 u0 = __ldg(Uc + (long long)X * T + Tt);
-    double2 u1 = __ldg(Uc + V + (long long)X * T + Tt);
-    double2 u0m = __ldg(Uc + (long long)gxm[i] * T + Tt);
-    double2 u1m = __ldg(Uc + V + (long long)X * T + gtm[j]);
-    Spinor r = wilson_site<false>(cc, xp, xm, tp, tm, u0, u0m, u1, u1m, a.diag);
-    sD[0][i * RT + j] = r.s0;
-    sD[1][i * RT + j] = r.s1;
+  auto nb = [&](int ri, int rj, int& kxp, int& kxm, int& ktp, int& ktm) {
+    const int ip = HX ? ri + 1 : (ri + 1 == RX ? 0 : ri + 1);
+    const int im = HX ? ri - 1 : (ri == 0 ? RX - 1 : ri - 1);
+    const int jp = HT ? rj + 1 : (rj + 1 == RT ? 0 : rj + 1);
+    const int jm = HT ? rj - 1 : (rj == 0 ? RT - 1 : rj - 1);
+    kxp = ip * RT + rj;
+    kxm = im * RT + rj;
+    ktp = ri * RT + jp;
+    ktm = ri * RT + jm;
+  };
+
+  // ---- phase B: t = D v on the tile + 1-site halo
+  constexpr int DX0 = HX / 2, DT0 = HT / 2;
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int k = threadIdx.x + j * NT;
+    if (k >= NR) continue;
+    const int ri = k / RT, rj = k - (k / RT) * RT;
+    if (ri < DX0 || ri >= RX - DX0 || rj < DT0 || rj >= RT - DT0) continue;
+    int kxp, kxm, ktp, ktm;
+    nb(ri, rj, kxp, kxm, ktp, ktm);
+    t[j] = res_consume<false>(E, NR, v[j], u0[j], u1[j], kxp, kxm, ktp, ktm, a.diag);
+  }
+  __syncthreads();   // every export of phase A consumed
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int k = threadIdx.x + j * NT;
+    if (k >= NR) continue;
+    const int ri = k / RT, rj = k - (k / RT) * RT;
+    if (ri < DX0 || ri >= RX - DX0 || rj < DT0 || rj >= RT - DT0) continue;
+    res_produce<true>(E, NR, k, t[j], u0[j], u1[j]);
   }
   __syncthreads();
 
-  // ---- stage 2: D^dag on the tile
+  // ---- phase C: D^dag on the tile
   double part = 0.0;
-  for (int k = threadIdx.x; k < TX * TT; k += NT) {
-    const int li = k / TT, lj = k - (k / TT) * TT;
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int k = threadIdx.x + j * NT;
+    if (k >= NR) continue;
+    const int ri = k / RT, rj = k - (k / RT) * RT;
+    const int li = ri - HX, lj = rj - HT;
+    if (li < 0 || li >= TX || lj < 0 || lj >= TT) continue;
     if (x0 + li >= L || t0 + lj >= T) continue;     // clipped tile
-    const int i = HX + li, j = HT + lj;
-    const int ip = HX ? i + 1 : (i + 1 == RX ? 0 : i + 1);
-    const int im = HX ? i - 1 : (i == 0 ? RX - 1 : i - 1);
-    const int jp = HT ? j + 1 : (j + 1 == RT ? 0 : j + 1);
-    const int jm = HT ? j - 1 : (j == 0 ? RT - 1 : j - 1);
-    Spinor cc{sD[0][i * RT + j], sD[1][i * RT + j]};
-    Spinor xp{sD[0][ip * RT + j], sD[1][ip * RT + j]};
-    Spinor xm{sD[0][im * RT + j], sD[1][im * RT + j]};
-    Spinor tp{sD[0][i * RT + jp], sD[1][i * RT + jp]};
-    Spinor tm{sD[0][i * RT + jm], sD[1][i * RT + jm]};
-    const int X = gx[i], Tt = gt[j];
-    double2 u0 = __ldg(Uc + (long long)X * T + Tt);
-    double2 u1 = __ldg(Uc + V + (long long)X * T + Tt);
-    double2 u0m = __ldg(Uc + (long long)gxm[i] * T + Tt);
-    double2 u1m = __ldg(Uc + V + (long long)X * T + gtm[j]);
-    Spinor r = wilson_site<true>(cc, xp, xm, tp, tm, u0, u0m, u1, u1m, a.diag);
-    const long long site = cbase + (long long)X * T + Tt;
+    int kxp, kxm, ktp, ktm;
+    nb(ri, rj, kxp, kxm, ktp, ktm);
+    Spinor r = res_consume<true>(E, NR, t[j], u0[j], u1[j], kxp, kxm, ktp, ktm, a.diag);
+    const long long site = cbase + (long long)gx[ri] * T + gt[rj];
     if (MODE == MODE_X) {
       Spinor bb = ld256_spinor_nc(a.bvec, site);
       r.s0 = csub(bb.s0, r.s0);
       r.s1 = csub(bb.s1, r.s1);
       part += spinor_norm2(r);
     } else if (MODE == MODE_P) {
-      Spinor pp{sA[0][i * RT + j], sA[1][i * RT + j]};
-      part += spinor_redot(pp, r);
+      part += spinor_redot(v[j], r);
     }
     st256_spinor(a.out, site, r);
   }
   if (MODE != MODE_PLAIN) {
     double s = block_sum<NT>(part, slot);
     if (threadIdx.x == 0) a.partial[(long long)c * a.tiles_per_chain + tile] = s;
+  }
+}
+
+// One CTA per tile.
+template <int TX, int TT, int HX, int HT, int MODE, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_normal_tile(TileArgs a) {
+  constexpr int RX = TX + 2 * HX, RT = TT + 2 * HT;
+  extern __shared__ double2 E[];            // [4][NR] exported projections (dynamic)
+  __shared__ int gx[RX], gxm[RX], gt[RT], gtm[RT];
+  __shared__ double slot[NT / 32];
+  const int c = blockIdx.x / a.tiles_per_chain;
+  const int tile = blockIdx.x - c * a.tiles_per_chain;
+  if (MODE != MODE_PLAIN && a.flag && a.flag[c] == 0) return;
+  tile_body<TX, TT, HX, HT, MODE, NT>(a, c, tile, E, gx, gxm, gt, gtm, slot);
+}
+
+// Persistent variant for sparse work (the CG true-residual pass, where only
+// flagged chains have anything to do): a fixed grid strides over tiles.
+template <int TX, int TT, int HX, int HT, int MODE, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_normal_tile_sparse(TileArgs a) {
+  constexpr int RX = TX + 2 * HX, RT = TT + 2 * HT;
+  extern __shared__ double2 E[];
+  __shared__ int gx[RX], gxm[RX], gt[RT], gtm[RT];
+  __shared__ double slot[NT / 32];
+  __shared__ unsigned mask;
+  const int ntiles = a.B * a.tiles_per_chain;
+  // chunks of 32 tiles: warp 0 reads the 32 flags in parallel, the CTA then
+  // walks the set bits (an idle pass costs one flag read per chunk)
+  for (int base = blockIdx.x * 32; base < ntiles; base += gridDim.x * 32) {
+    if (threadIdx.x < 32) {
+      const int w = base + threadIdx.x;
+      const bool f = w < ntiles && a.flag[w / a.tiles_per_chain] != 0;
+      const unsigned m = __ballot_sync(0xffffffffu, f);
+      if (threadIdx.x == 0) mask = m;
+    }
+    __syncthreads();
+    unsigned m = mask;
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      const int w = base + bit;
+      const int c = w / a.tiles_per_chain;
+      tile_body<TX, TT, HX, HT, MODE, NT>(a, c, w - c * a.tiles_per_chain, E, gx, gxm, gt, gtm, slot);
+      __syncthreads();   // shared-memory readers of this tile are done
+    }
+    __syncthreads();     // everyone has read `mask`
   }
 }
 
@@ -155,22 +212,41 @@ struct TileShape {
 inline TileShape pick_tile(int L, int T) {
   TileShape s;
   if (L == 16 && T == 16) s = {0, 16, 16, 1, 1};
-  else if (T == 32 && L % 8 == 0) s = {1, 8, 32, L / 8, 1};
-  else if (T == 64 && L % 4 == 0) s = {2, 4, 64, L / 4, 1};
-  else if (T % 32 == 0 && L % 8 == 0 && T > 64) s = {3, 8, 32, L / 8, T / 32};
+  else if (T == 32 && L % 16 == 0) s = {1, 16, 32, L / 16, 1};
+  else if (T == 64 && L % 8 == 0) s = {2, 8, 64, L / 8, 1};
+  else if (T % 64 == 0 && L % 16 == 0 && T > 64) s = {3, 16, 64, L / 16, T / 64};
   else s = {4, 8, 16, (L + 7) / 8, (T + 15) / 16};
   return s;
 }
 
-// Launch k_normal_tile with the instantiation matching `sh`.
+template <int TX, int TT, int HX, int HT, int MODE, int NT, int MINB>
+inline void launch_tile_inst(const TileArgs& a, cudaStream_t st, int sparse_grid) {
+  constexpr int NR = (TX + 2 * HX) * (TT + 2 * HT);
+  constexpr size_t smem = sizeof(double2) * 4 * NR;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_normal_tile<TX, TT, HX, HT, MODE, NT, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_normal_tile_sparse<TX, TT, HX, HT, MODE, NT, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  if (sparse_grid > 0)
+    k_normal_tile_sparse<TX, TT, HX, HT, MODE, NT, MINB><<<sparse_grid, NT, smem, st>>>(a);
+  else
+    k_normal_tile<TX, TT, HX, HT, MODE, NT, MINB><<<(unsigned)a.B * a.tiles_per_chain, NT, smem, st>>>(a);
+}
+
+// Launch the instantiation matching `sh`.  sparse_grid > 0 selects the
+// persistent flag-skipping variant with that many CTAs.
 template <int MODE>
-inline void launch_normal_tile(const TileShape& sh, const TileArgs& a, cudaStream_t st) {
-  const unsigned grid = (unsigned)a.B * a.tiles_per_chain;
+inline void launch_normal_tile(const TileShape& sh, const TileArgs& a, cudaStream_t st,
+                               int sparse_grid = 0) {
   switch (sh.kind) {
-    case 0: k_normal_tile<16, 16, 0, 0, MODE, 256><<<grid, 256, 0, st>>>(a); break;
-    case 1: k_normal_tile<8, 32, 2, 0, MODE, 256><<<grid, 256, 0, st>>>(a); break;
-    case 2: k_normal_tile<4, 64, 2, 0, MODE, 256><<<grid, 256, 0, st>>>(a); break;
-    case 3: k_normal_tile<8, 32, 2, 2, MODE, 256><<<grid, 256, 0, st>>>(a); break;
-    default: k_normal_tile<8, 16, 2, 2, MODE, 128><<<grid, 128, 0, st>>>(a); break;
+    case 0: launch_tile_inst<16, 16, 0, 0, MODE, 256, 3>(a, st, sparse_grid); break;
+    case 1: launch_tile_inst<16, 32, 2, 0, MODE, 512, 2>(a, st, sparse_grid); break;
+    case 2: launch_tile_inst<8, 64, 2, 0, MODE, 512, 2>(a, st, sparse_grid); break;
+    case 3: launch_tile_inst<16, 64, 2, 2, MODE, 512, 2>(a, st, sparse_grid); break;
+    default: launch_tile_inst<8, 16, 2, 2, MODE, 128, 4>(a, st, sparse_grid); break;
   }
 }

@@ -84,6 +84,8 @@ def main():
         B, L = 4096, 32
         q, psi = field(B, L, 3)
         op = sw.WilsonDirac(q, 0.1)
+        F.cg_solve(op, psi, 1e-10, maxiter=60, stop="batch_global")   # load every kernel
+        torch.cuda.synchronize()
         F.CG_PROFILE = []
         F.cg_solve(op, psi, 1e-10, stop="batch_global")
         torch.cuda.synchronize()
