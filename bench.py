@@ -45,6 +45,12 @@ sys.path.insert(0, str(ROOT))
 PEAKS_PATH = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
 
+# DRAM bytes per lattice site of one resident-CG launch, measured by ncu
+# (profiles/r01/ncu_full_k_cg_resident.txt: 33.627136 MB read + 38.912 KB
+# written for 2048 chains x 256 sites): U and b in, x out — the solve itself
+# never leaves the SM.
+NCU_CG_DRAM_BYTES_PER_SITE = (33.627136e6 + 38.912e3) / (2048 * 256)
+
 CFG3 = dict(L=16, T=16, beta=2.0, m0=0.1, tau=1.0, scheme="adapted-nested-fg", micro_per_call=2,
             cg_tol=1e-10)
 
@@ -316,10 +322,12 @@ def run_ours(args):
     if rank == 0 and not args.no_stencil:   # fresh allocator / caches
         stencil = stencil_bench(torch, sw, _lib, hbm_peak)
 
-    chains = args.chains
+    from paper_1512_03812_b200.ensemble import gather_observables, shard_chains, summarize
+    shard = shard_chains(args.chains * world, world, rank)   # weak scaling: chains per GPU fixed
+    chains = shard.count
     cfg = sw.HmcConfig(h=1.0 / args.outer, **CFG3)
     geom = sw.LatticeGeom(cfg.L, cfg.T)
-    drng = sw.DeviceRng(seed=2024, stream0=rank * chains)
+    drng = sw.DeviceRng(seed=2024, stream0=shard.start)     # chain c <-> Philox key (seed, c)
     q = sw.hot_start(sw.make_rng(2024, rank), geom, batch=chains)
 
     for _ in range(args.warmup):
@@ -337,8 +345,8 @@ def run_ours(args):
     e0.record()
     for _ in range(args.steps):
         q, st = sw.hmc_update_ensemble(q, cfg, device_rng=drng)
-        acc.append(st.accepted.mean())
-        dhs.append(np.abs(st.dh).mean())
+        acc.append(st.accepted)
+        dhs.append(st.dh)
     e1.record()
     torch.cuda.synchronize()
     barrier()
@@ -365,12 +373,11 @@ def run_ours(args):
     solves_per_traj = n_solves / args.steps
 
     # ensemble observables: one NCCL all-gather at the end (the only collective)
-    acc_rate = float(np.mean(acc))
-    if world > 1:
-        t = torch.tensor([acc_rate, float(np.mean(dhs))], dtype=torch.float64, device="cuda")
-        allv = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(allv, t)
-        acc_rate = float(np.mean([v[0].item() for v in allv]))
+    obs = gather_observables({"dh": np.concatenate(dhs),
+                              "accepted": np.concatenate(acc).astype(np.float64)},
+                             shard_chains(shard.total * args.steps, world, rank))
+    ens = summarize(obs)
+    acc_rate = ens["acceptance"]
 
     # e2e through the public API with host buffers
     e2e = None
@@ -412,11 +419,19 @@ def run_ours(args):
                        "chains_per_gpu": chains, "global_chains": chains * world,
                        "parallelism": f"chain-ensemble dp{world}",
                        "l2": "working set > L2 (126 MB); no flush needed",
-                       "acceptance": acc_rate, "cg_solves_per_traj": solves_per_traj,
+                       "acceptance": acc_rate, "mean_abs_dh": ens["mean_abs_dh"],
+                       "exp_minus_dh": ens["exp_minus_dh"],
+                       "cg_solves_per_traj": solves_per_traj,
                        "inversions_per_traj_reference_convention": st.inversions,
                        "cg_iterations_per_chain_traj": cg_iters / (chains * args.steps)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None,
+                         "frac": achieved / hbm_peak,
+                         "traffic": NCU_CG_DRAM_BYTES_PER_SITE * V * chains,
+                         "traffic_source": "dram__bytes_read.sum+dram__bytes_write.sum of one "
+                                           "k_cg_resident launch (ncu --set full, 2048 chains, "
+                                           "profiles/r01/ncu_full_k_cg_resident.txt), per site, "
+                                           "x sites of one launch here",
+                         "algorithmic_bytes_per_launch": cg_bytes / max(1, n_solves),
                          "peak_kind": peak_kind,
                          "kernel": "k_cg_resident (per-chain CG, one CTA per chain)",
                          "bytes_model": "352 B/site/CG-iteration (SURVEY 8(d)), "

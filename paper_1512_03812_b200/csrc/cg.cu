@@ -40,47 +40,45 @@ constexpr int kReplace = kResReplace;   // residual replacement period (fermion.
 // ============================================================ resident CG
 // (kernel in resident.cuh)
 
-template <int NT, int SPT>
+template <int NT, int SPT, int MINB>
 int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
   const size_t smem = sizeof(double2) * 8 * (size_t)a.L * a.T;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cg_resident<NT, SPT>,
+    cudaError_t e = cudaFuncSetAttribute(k_cg_resident<NT, SPT, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  k_cg_resident<NT, SPT><<<B, NT, smem, ctx->stream>>>(a);
+  k_cg_resident<NT, SPT, MINB><<<B, NT, smem, ctx->stream>>>(a);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
 
-// Threads x sites-per-thread of the resident engine for V sites.  The
-// SCH_RESIDENT environment variable ("NTxSPT", e.g. "128x2") overrides the
-// default for tuning runs.
+// Threads x sites-per-thread x min-CTAs-per-SM of the resident engine for V
+// sites.  SCH_RESIDENT ("NTxSPTxMINB", e.g. "128x2x4") overrides the default
+// for tuning runs.
 int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
-  static int forced_nt = -1, forced_spt = -1;
-  if (forced_nt < 0) {
-    forced_nt = forced_spt = 0;
-    if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%d", &forced_nt, &forced_spt);
+  static int fnt = -1, fspt = 0, fminb = 0;
+  if (fnt < 0) {
+    fnt = 0;
+    if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%dx%d", &fnt, &fspt, &fminb);
   }
-  int nt = 0, spt = 0;
-  if (forced_nt > 0 && (long long)forced_nt * forced_spt >= V) {
-    nt = forced_nt;
-    spt = forced_spt;
-  } else if (V <= 128) { nt = 128; spt = 1; }
-  else if (V <= 256) { nt = 128; spt = 2; }
-  else if (V <= 512) { nt = 256; spt = 2; }
-  else { nt = 256; spt = 4; }
-  if (nt == 128 && spt == 1) return launch_resident<128, 1>(ctx, a, B);
-  if (nt == 128 && spt == 2) return launch_resident<128, 2>(ctx, a, B);
-  if (nt == 256 && spt == 1) return launch_resident<256, 1>(ctx, a, B);
-  if (nt == 256 && spt == 2) return launch_resident<256, 2>(ctx, a, B);
-  if (nt == 256 && spt == 4) return launch_resident<256, 4>(ctx, a, B);
-  if (nt == 512 && spt == 1) return launch_resident<512, 1>(ctx, a, B);
-  if (nt == 512 && spt == 2) return launch_resident<512, 2>(ctx, a, B);
-  if (nt == 1024 && spt == 1) return launch_resident<1024, 1>(ctx, a, B);
-  return sch_fail(ctx, SCH_ERR_ARG, "no resident CG instantiation %dx%d", nt, spt);
+  int nt, spt, minb;
+  if (fnt > 0 && (long long)fnt * fspt >= V) { nt = fnt; spt = fspt; minb = fminb; }
+  else if (V <= 128) { nt = 128; spt = 1; minb = 1; }
+  else if (V <= 256) { nt = 128; spt = 2; minb = 4; }
+  else if (V <= 512) { nt = 256; spt = 2; minb = 1; }
+  else { nt = 256; spt = 4; minb = 1; }
+#define SCH_RES(N, S, M) \
+  if (nt == N && spt == S && minb == M) return launch_resident<N, S, M>(ctx, a, B);
+  SCH_RES(128, 1, 1) SCH_RES(128, 1, 6) SCH_RES(128, 1, 8)
+  SCH_RES(128, 2, 1) SCH_RES(128, 2, 4) SCH_RES(128, 2, 5) SCH_RES(128, 2, 6)
+  SCH_RES(256, 1, 1) SCH_RES(256, 1, 3) SCH_RES(256, 1, 4)
+  SCH_RES(256, 2, 1) SCH_RES(256, 2, 2) SCH_RES(256, 2, 3)
+  SCH_RES(256, 4, 1) SCH_RES(512, 2, 1) SCH_RES(512, 1, 1)
+#undef SCH_RES
+  return sch_fail(ctx, SCH_ERR_ARG, "no resident CG instantiation %dx%dx%d", nt, spt, minb);
 }
 
 // =========================================================== streaming CG

@@ -84,8 +84,8 @@ SCH_DEV Spinor sp_sub(const Spinor& a, const Spinor& b) {
   return r;
 }
 
-template <int NT, int SPT>
-__global__ void __launch_bounds__(NT) k_cg_resident(ResArgs a) {
+template <int NT, int SPT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
   extern __shared__ double2 sm[];
   __shared__ double red[3][NT / 32];
   const int L = a.L, T = a.T, V = L * T;
