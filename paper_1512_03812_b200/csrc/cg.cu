@@ -28,6 +28,7 @@
 #include "common.cuh"
 #include "runtime.hpp"
 #include "tile.cuh"
+#include "tma_tile.cuh"
 #include "resident.cuh"
 #include <cstdio>
 #include <cstdlib>
@@ -420,7 +421,7 @@ __global__ void k_zero_x_if_null(ElemArgs e, StreamState st) {
 int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, const double2* x0,
                  int B, int L, int T, double m0, double tol, int maxiter, int global_mode, int* iters,
                  double* relres, int* status) {
-  const TileShape sh = pick_tile(L, T);
+  const TileShape sh = pick_tile(L, T, use_tma_cg());
   const int tpc = sh.tiles_x * sh.tiles_t;
   const long long V = (long long)L * T;
   const size_t nvec = (size_t)B * V * 2;   // double2 per vector
@@ -496,6 +497,10 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
   const bool pt = tpc <= kSmallTpc;
   const unsigned cgrid = pt ? blocks_for(B, 128) : (unsigned)B;
   const int sparse = ctx->num_sms * 2;   // persistent grid of the true-residual pass
+  // TMA-pipelined stencil pass when its tiling equals the elementwise tiling
+  int tma_tx = 0;
+  const bool tma_p = use_tma_cg() && tma_tile_shape(L, T, tma_tx) && tma_tx == sh.TX &&
+                     sh.tiles_t == 1;
   if (pt) k_ctrl_init<true><<<cgrid, 128, 0, s>>>(st, x0 != nullptr);
   else k_ctrl_init<false><<<cgrid, 128, 0, s>>>(st, x0 != nullptr);
   SCH_LAUNCHED(ctx);
@@ -522,7 +527,8 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
     int n = std::min(chunk, maxiter - it + 1);
     for (int j = 0; j < n; ++j, ++it) {
       const int repl = (it % kReplace) == 0;
-      launch_normal_tile<MODE_P>(sh, tp, s);
+      if (tma_p) launch_normal_tma<MODE_P>(tp, s, ctx->num_sms);
+      else launch_normal_tile<MODE_P>(sh, tp, s);
       SCH_LAUNCHED(ctx);
       if (pt) {
         k_cg_update<true><<<ngrid, 256, 0, s>>>(e, st, repl);

@@ -6,6 +6,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -91,3 +92,25 @@ inline int sch_workspace(sch_ctx* c, size_t bytes, void** out) {
 }
 
 inline unsigned blocks_for(long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
+
+// The TMA-pipelined stencil is the default where its tile shapes apply;
+// SCH_NO_TMA=1 selects the plain per-tile kernels (A/B measurements).
+inline bool use_tma() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCH_NO_TMA");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// The streaming CG's stencil pass measured faster with the per-tile kernel
+// (profiles/r01/README.md); SCH_TMA_CG=1 switches it to the TMA pipeline.
+inline bool use_tma_cg() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCH_TMA_CG");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1 && use_tma();
+}

@@ -209,8 +209,21 @@ struct TileShape {
   int tiles_x, tiles_t;
 };
 
-inline TileShape pick_tile(int L, int T) {
+inline bool tma_tile_shape(int L, int T, int& TX);   // tma_tile.cuh
+inline bool use_tma();                                 // runtime.hpp
+
+// `tma`: the caller will run the TMA-pipelined stencil, so every pass of the
+// streaming CG must use its tiling for the per-tile partials to line up.
+inline TileShape pick_tile(int L, int T, bool tma = false) {
   TileShape s;
+  int tx = 0;
+  if (tma && tma_tile_shape(L, T, tx)) {
+    if (T == 32 && tx == 16) return {1, 16, 32, L / 16, 1};
+    if (T == 32 && tx == 8) return {5, 8, 32, L / 8, 1};
+    if (T == 32 && tx == 4) return {8, 4, 32, L / 4, 1};
+    if (T == 16 && tx == 16) return {6, 16, 16, L / 16, 1};
+    if (T == 64 && tx == 4) return {7, 4, 64, L / 4, 1};
+  }
   if (L == 16 && T == 16) s = {0, 16, 16, 1, 1};
   else if (T == 32 && L % 16 == 0) s = {1, 16, 32, L / 16, 1};
   else if (T == 64 && L % 8 == 0) s = {2, 8, 64, L / 8, 1};
@@ -247,6 +260,10 @@ inline void launch_normal_tile(const TileShape& sh, const TileArgs& a, cudaStrea
     case 1: launch_tile_inst<16, 32, 2, 0, MODE, 512, 2>(a, st, sparse_grid); break;
     case 2: launch_tile_inst<8, 64, 2, 0, MODE, 512, 2>(a, st, sparse_grid); break;
     case 3: launch_tile_inst<16, 64, 2, 2, MODE, 512, 2>(a, st, sparse_grid); break;
+    case 5: launch_tile_inst<8, 32, 2, 0, MODE, 384, 2>(a, st, sparse_grid); break;
+    case 6: launch_tile_inst<16, 16, 2, 0, MODE, 320, 2>(a, st, sparse_grid); break;
+    case 7: launch_tile_inst<4, 64, 2, 0, MODE, 512, 2>(a, st, sparse_grid); break;
+    case 8: launch_tile_inst<4, 32, 2, 0, MODE, 256, 3>(a, st, sparse_grid); break;
     default: launch_tile_inst<8, 16, 2, 2, MODE, 128, 4>(a, st, sparse_grid); break;
   }
 }

@@ -4,6 +4,7 @@
 #include "common.cuh"
 #include "runtime.hpp"
 #include "tile.cuh"
+#include "tma_tile.cuh"
 #include "../../include/schwinger_sm100.h"
 
 namespace {
@@ -288,7 +289,6 @@ int sch_ddagd(sch_ctx* ctx, const double* U, const double* psi, double* out, int
               double m0) {
   SCH_CHECK_ARG(ctx, U && psi && out && B >= 1 && L >= 2 && T >= 2, "ddagd: bad args");
   SCH_CHECK_ARG(ctx, psi != out, "ddagd: in-place application is not supported");
-  TileShape sh = pick_tile(L, T);
   TileArgs a{};
   a.U = (const double2*)U;
   a.in = (const double2*)psi;
@@ -296,10 +296,18 @@ int sch_ddagd(sch_ctx* ctx, const double* U, const double* psi, double* out, int
   a.B = B;
   a.L = L;
   a.T = T;
-  a.tiles_t = sh.tiles_t;
-  a.tiles_per_chain = sh.tiles_x * sh.tiles_t;
   a.diag = 2.0 + m0;
-  launch_normal_tile<MODE_PLAIN>(sh, a, ctx->stream);
+  int TX = 0;
+  if (use_tma() && tma_tile_shape(L, T, TX)) {   // persistent TMA-pipelined tiles
+    a.tiles_t = 1;
+    a.tiles_per_chain = L / TX;
+    launch_normal_tma<MODE_PLAIN>(a, ctx->stream, ctx->num_sms);
+  } else {
+    TileShape sh = pick_tile(L, T);
+    a.tiles_t = sh.tiles_t;
+    a.tiles_per_chain = sh.tiles_x * sh.tiles_t;
+    launch_normal_tile<MODE_PLAIN>(sh, a, ctx->stream);
+  }
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }

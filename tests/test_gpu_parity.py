@@ -44,6 +44,23 @@ def test_stencil_matches_reference(sw, golden, case):
     assert rel_err(npy(op.normal(psi)), g[f"{case}_DdD"]) < TOL_OP
 
 
+@pytest.mark.parametrize("B,L,T", [(3, 32, 16), (2, 8, 64), (5, 48, 32), (1, 16, 32)])
+def test_tma_stencil_shapes_match_oracle(sw, B, L, T):
+    """Shapes served by the TMA-pipelined D^dag D (whole time rows) and by the
+    streaming CG's TMA stencil pass, against the oracle."""
+    from oracle import schwinger_oracle as O
+    rng = np.random.default_rng(L * T + B)
+    q = rng.uniform(-np.pi, np.pi, (B, 2, L, T))
+    psi = rng.standard_normal((B, L, T, 2)) + 1j * rng.standard_normal((B, L, T, 2))
+    op = sw.WilsonDirac(q, 0.1)
+    ref = O.normal_op(O.fermion_links(q), psi, 0.1)
+    assert rel_err(npy(op.normal(psi)), ref) < TOL_OP
+    x, it, _ = sw.cg_normal(op, psi, 1e-10, stop="batch_global")
+    xo, ito, _ = O.cg_normal(O.fermion_links(q), 0.1, psi, 1e-10, stop="batch_global")
+    assert it == ito
+    assert rel_err(npy(x), xo) < TOL_OP
+
+
 def test_reference_stencil_kats(sw):
     """Free constant mode and point-source stencil (reference test_fermion.py:25-48)."""
     q = np.zeros((2, 4, 4))
