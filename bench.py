@@ -54,6 +54,14 @@ NCU_CG_DRAM_BYTES_PER_SITE = (33.627136e6 + 38.912e3) / (2048 * 256)
 CFG3 = dict(L=16, T=16, beta=2.0, m0=0.1, tau=1.0, scheme="adapted-nested-fg", micro_per_call=2,
             cg_tol=1e-10)
 
+# BASELINE.json configs[2] (the bench line) and configs[3] (light fermions)
+WORKLOADS = {
+    "cfg3": dict(chains=8192, outer=4, phys=CFG3),
+    "cfg4": dict(chains=1024, outer=8,
+                 phys=dict(L=64, T=64, beta=4.0, m0=0.02, tau=1.0, scheme="adapted-nested-fg",
+                           micro_per_call=4, cg_tol=1e-10)),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -61,13 +69,23 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--chains", type=int, default=8192, help="chains per GPU")
-    ap.add_argument("--outer", type=int, default=4, help="outer (fermion) steps per trajectory")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3",
+                    help="cfg3 (default, the bench line) or cfg4 (64^2 light-fermion ensemble)")
+    ap.add_argument("--chains", type=int, default=None, help="chains per GPU")
+    ap.add_argument("--outer", type=int, default=None, help="outer (fermion) steps per trajectory")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stencil", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    args = ap.parse_args()
+    w = WORKLOADS[args.workload]
+    if args.chains is None:
+        args.chains = w["chains"]
+    if args.outer is None:
+        args.outer = w["outer"]
+    global CFG3
+    CFG3 = dict(w["phys"])
+    return args
 
 
 def peaks():
@@ -414,8 +432,9 @@ def run_ours(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64/c128", "data": "synthetic (hot start, device Philox heatbaths)",
-            "config": {"workload": "cfg3: independent 16x16 chains, beta=2.0, m0=0.1, tau=1, "
-                                   f"adapted-nested-fg {args.outer}x2 steps (h={1.0 / args.outer}), "
+            "config": {"workload": f"{args.workload}: independent {cfg.L}x{cfg.T} chains, "
+                                   f"beta={cfg.beta}, m0={cfg.m0}, tau={cfg.tau}, adapted-nested-fg "
+                                   f"{args.outer}x{cfg.micro_per_call} steps (h={1.0 / args.outer}), "
                                    "CG tol 1e-10 per-chain stop, complex128",
                        "chains_per_gpu": chains, "global_chains": chains * world,
                        "parallelism": f"chain-ensemble dp{world}",
