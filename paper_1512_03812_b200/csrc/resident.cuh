@@ -53,8 +53,10 @@ SCH_DEV void res_produce(double2* __restrict__ E, int V, int s, const Spinor& v,
   }
 }
 
-// consumer: (D v)(n) or (D^dag v)(n) from the neighbours' exports
-template <bool DAG>
+// consumer: (D v)(n) or (D^dag v)(n) from the neighbours' exports.
+// PRESCALED: the links were multiplied by -1/2 once (exact in binary), so the
+// four hops arrive already scaled and the site term is one FMA per component.
+template <bool DAG, bool PRESCALED = false>
 SCH_DEV Spinor res_consume(const double2* __restrict__ E, int V, const Spinor& v, double2 u0,
                            double2 u1, int nxp, int nxm, int ntp, int ntm, double diag) {
   const double2 hf0 = cmul(u0, E[nxp]);
@@ -65,8 +67,13 @@ SCH_DEV Spinor res_consume(const double2* __restrict__ E, int V, const Spinor& v
   double2 o1 = DAG ? cadd(csub(hf0, hb0), cmuli(csub(hf1, hb1)))
                    : cadd(csub(hb0, hf0), cmuli(csub(hb1, hf1)));
   Spinor r;
-  r.s0 = make_double2(diag * v.s0.x - 0.5 * o0.x, diag * v.s0.y - 0.5 * o0.y);
-  r.s1 = make_double2(diag * v.s1.x - 0.5 * o1.x, diag * v.s1.y - 0.5 * o1.y);
+  if (PRESCALED) {
+    r.s0 = make_double2(__fma_rn(diag, v.s0.x, o0.x), __fma_rn(diag, v.s0.y, o0.y));
+    r.s1 = make_double2(__fma_rn(diag, v.s1.x, o1.x), __fma_rn(diag, v.s1.y, o1.y));
+  } else {
+    r.s0 = make_double2(diag * v.s0.x - 0.5 * o0.x, diag * v.s0.y - 0.5 * o0.y);
+    r.s1 = make_double2(diag * v.s1.x - 0.5 * o1.x, diag * v.s1.y - 0.5 * o1.y);
+  }
   return r;
 }
 
@@ -110,8 +117,8 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
       nxm[k] = (xx == 0 ? L - 1 : xx - 1) * T + tt;
       ntp[k] = xx * T + (tt + 1 == T ? 0 : tt + 1);
       ntm[k] = xx * T + (tt == 0 ? T - 1 : tt - 1);
-      u0[k] = __ldg(a.U + 2 * cb + s);
-      u1[k] = __ldg(a.U + 2 * cb + V + s);
+      u0[k] = cscale(-0.5, __ldg(a.U + 2 * cb + s));        // exact: power-of-two scale
+      u1[k] = cscale(-0.5, __ldg(a.U + 2 * cb + V + s));
       r[k] = ldg_spinor(a.b, cb + s);
       bb += spinor_norm2(r[k]);
     } else {
@@ -146,8 +153,8 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
       if (site[k] >= 0) {
-        Spinor t = res_consume<false>(E0, V, v[k], u0[k], u1[k], nxp[k], nxm[k], ntp[k], ntm[k],
-                                      a.diag);
+        Spinor t = res_consume<false, true>(E0, V, v[k], u0[k], u1[k], nxp[k], nxm[k], ntp[k],
+                                            ntm[k], a.diag);
         out[k] = t;
         res_produce<true>(E1, V, site[k], t, u0[k], u1[k]);
       }
@@ -155,8 +162,8 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
       if (site[k] >= 0)
-        out[k] = res_consume<true>(E1, V, out[k], u0[k], u1[k], nxp[k], nxm[k], ntp[k], ntm[k],
-                                   a.diag);
+        out[k] = res_consume<true, true>(E1, V, out[k], u0[k], u1[k], nxp[k], nxm[k], ntp[k],
+                                         ntm[k], a.diag);
   };
 
   Spinor w[SPT];   // A applied to something
