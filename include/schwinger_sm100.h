@@ -147,6 +147,33 @@ int sch_rng_normal(sch_ctx* ctx, double* out, int B, long long per_chain, uint64
 int sch_rng_uniform(sch_ctx* ctx, double* out, int B, long long per_chain, uint64_t seed,
                     uint64_t stream0, uint64_t ctr);
 
+/* ---- domain decomposition of one lattice (BASELINE configs[4]) -------- */
+/* One lattice split into G = nranks * strips_local x-strips of Lloc = L/G
+ * rows.  Fields are "extended strips": [strips_local][Lloc+4][T] (2 halo
+ * rows per side) in the usual per-site layouts.  nranks == 1: every strip in
+ * this process, halo exchange by a copy kernel.  nranks > 1: one strip per
+ * rank, NCCL send/recv of the 2-row faces and NCCL all-reduce of the CG
+ * scalars (libnccl.so.2 bound at run time). */
+typedef struct sch_dd sch_dd;
+int sch_nccl_unique_id(sch_ctx* ctx, void* id_out /* 128 bytes */);
+int sch_dd_create(sch_ctx* ctx, const void* nccl_id, int nranks, int rank, int L, int T,
+                  int strips_local, sch_dd** out);
+int sch_dd_destroy(sch_dd* dd);
+/* out4 = {strips_local, Lloc, Lext, G} */
+int sch_dd_geometry(const sch_dd* dd, int* out4);
+/* refresh the halo rows of a field [S][planes][Lext][T][words_per_site] (doubles) */
+int sch_dd_exchange(sch_ctx* ctx, sch_dd* dd, double* field, int planes, int words_per_site);
+/* out = D^dag D psi on the own rows (psi's halos are refreshed first);
+ * WilsonDirac.normal (fermion.py:129-131) on a decomposed lattice */
+int sch_dd_ddagd(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* psi_ext, double* out_ext,
+                 double m0);
+/* cg_normal (fermion.py:171-217) on a decomposed lattice; b's (and x0's)
+ * halos are refreshed in place.  Synchronises; host outputs may be NULL.
+ * Returns 3 when maxiter is hit. */
+int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ext, double* x_ext,
+                     double* x0_ext, double m0, double tol, int maxiter, int* h_iters,
+                     double* h_relres, int* h_status);
+
 /* ---- measurement probe (bench.py) ------------------------------------ */
 /* FP64 FMA issue-rate probe: blocks x 256 threads x iters x 32 DFMA
  * (flops = blocks*256*iters*64); scratch needs `blocks` doubles. */

@@ -61,6 +61,15 @@ _SIGNATURES = {
     "sch_select_chains": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_int, _c_ll],
     "sch_metropolis": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_int],
     "sch_probe_fp64": [_c_ptr, _c_ptr, _c_int, _c_int],
+    "sch_nccl_unique_id": [_c_ptr, _c_ptr],
+    "sch_dd_create": [_c_ptr, _c_ptr, _c_int, _c_int, _c_int, _c_int, _c_int,
+                      ctypes.POINTER(_c_ptr)],
+    "sch_dd_destroy": [_c_ptr],
+    "sch_dd_geometry": [_c_ptr, ctypes.POINTER(_c_int)],
+    "sch_dd_exchange": [_c_ptr, _c_ptr, _c_ptr, _c_int, _c_int],
+    "sch_dd_ddagd": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_dbl],
+    "sch_dd_cg_normal": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_int,
+                         ctypes.POINTER(_c_int), ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_int)],
 }
 _RESTYPES = {"sch_last_error": ctypes.c_char_p, "sch_launch_count": ctypes.c_ulonglong,
              "sch_build_info": ctypes.c_char_p}

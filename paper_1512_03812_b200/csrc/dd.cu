@@ -1,0 +1,532 @@
+// Domain decomposition of ONE lattice into x-strips (BASELINE configs[4],
+// SURVEY §8(e) mode 2): halo exchange inside every D^dag D application and
+// global reductions inside every CG iteration.
+//
+// Layout: each strip holds its Lloc own rows plus H = 2 halo rows on each
+// side (the fused D^dag D reaches two sites), as an "extended strip" of
+// Lext = Lloc + 4 rows x T:
+//     rows 0,1            <- rows Lloc, Lloc+1 of the left neighbour strip
+//     rows 2 .. Lloc+1    own rows (global rows x0 .. x0+Lloc-1)
+//     rows Lloc+2, Lloc+3 <- rows 2, 3 of the right neighbour strip
+// so an x-face is a contiguous run of T sites and the exchange is zero-copy.
+// The stencil kernels run unchanged on the extended strip; rows outside the
+// own range are masked out of outputs and reductions.
+//
+// Transports:
+//   local : all S strips live in this process as a batch [S][Lext][T]; the
+//           exchange is one copy kernel, reductions are plain sums (this is
+//           how the path is exercised on one GPU);
+//   nccl  : one strip per rank; ncclSend/ncclRecv of the 2-row faces with
+//           the +-x neighbours (grouped), ncclAllReduce of the CG scalars.
+//           libnccl.so.2 is bound at run time (dlopen), so the library still
+//           loads on machines without NCCL.
+//
+// CG semantics are the reference's (fermion.py:171-217) for a single chain.
+// p and x are updated on halo rows too (from exchanged r and their own
+// previous halos, bit-identical to the owner's values), so each iteration
+// exchanges only r.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "runtime.hpp"
+#include "tile.cuh"
+#include "../../include/schwinger_sm100.h"
+
+namespace {
+
+constexpr int kHalo = 2;
+constexpr int kDDReplace = 50;
+constexpr int kRedGrid = 296;   // fixed grid of the elementwise passes (deterministic partials)
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (api.h) {
+      auto sym = [&](const char* n) { return dlsym(api.h, n); };
+      api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+      api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+      api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+      api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+      api.Send = (decltype(api.Send))sym("ncclSend");
+      api.Recv = (decltype(api.Recv))sym("ncclRecv");
+      api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+      api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart &&
+               api.GroupEnd && api.Send && api.Recv && api.AllReduce;
+    }
+  }
+  return api;
+}
+
+#define SCH_NCCL(ctx, expr)                                                               \
+  do {                                                                                    \
+    ncclResult_t _r = (expr);                                                             \
+    if (_r != ncclSuccess)                                                                \
+      return sch_fail((ctx), SCH_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr,     \
+                      nccl().GetErrorString ? nccl().GetErrorString(_r) : "nccl error");  \
+  } while (0)
+
+}  // namespace
+
+struct sch_dd {
+  int nranks = 1, rank = 0;   // transport ranks
+  int S = 1;                  // strips held by this process
+  int G = 1;                  // strips in the whole lattice
+  int L = 0, T = 0, Lloc = 0, Lext = 0;
+  ncclComm_t comm = nullptr;  // null => local transport
+};
+
+namespace {
+
+// ---------------------------------------------------------- halo exchange
+// Field layout [S][P planes][Lext][T][W doubles]; copy the 4 halo rows of
+// every strip from its periodic neighbours (local transport).
+__global__ void k_dd_exchange_local(double* __restrict__ f, int S, int P, int Lext, int Lloc, int T,
+                                    int W) {
+  const long long row = (long long)T * W;
+  const long long n = (long long)S * P * 4 * row;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i % row;
+    long long q = i / row;
+    const int h = (int)(q % 4);
+    q /= 4;
+    const int pl = (int)(q % P);
+    const int s = (int)(q / P);
+    // destination halo row and its source strip/row
+    int dst_row, src_strip, src_row;
+    if (h < 2) {                    // rows 0,1 <- left's Lloc, Lloc+1
+      dst_row = h;
+      src_strip = (s - 1 + S) % S;
+      src_row = Lloc + h;
+    } else {                        // rows Lloc+2, Lloc+3 <- right's 2, 3
+      dst_row = Lloc + h;
+      src_strip = (s + 1) % S;
+      src_row = h;
+    }
+    const long long plane = (long long)Lext * row;
+    f[((long long)s * P + pl) * plane + dst_row * row + e] =
+        f[((long long)src_strip * P + pl) * plane + src_row * row + e];
+  }
+}
+
+int dd_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
+  if (dd->comm == nullptr) {
+    const long long n = (long long)dd->S * P * 4 * dd->T * W;
+    unsigned grid = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
+    k_dd_exchange_local<<<grid, 256, 0, ctx->stream>>>(f, dd->S, P, dd->Lext, dd->Lloc, dd->T, W);
+    SCH_LAUNCHED(ctx);
+    return SCH_OK;
+  }
+  NcclApi& n = nccl();
+  const int left = (dd->rank - 1 + dd->nranks) % dd->nranks;
+  const int right = (dd->rank + 1) % dd->nranks;
+  const size_t face = (size_t)2 * dd->T * W;   // two rows
+  const size_t row = (size_t)dd->T * W;
+  const size_t plane = (size_t)dd->Lext * row;
+  SCH_NCCL(ctx, n.GroupStart());
+  for (int pl = 0; pl < P; ++pl) {
+    double* base = f + pl * plane;
+    SCH_NCCL(ctx, n.Send(base + dd->Lloc * row, face, ncclDouble, right, dd->comm, ctx->stream));
+    SCH_NCCL(ctx, n.Recv(base, face, ncclDouble, left, dd->comm, ctx->stream));
+    SCH_NCCL(ctx, n.Send(base + 2 * row, face, ncclDouble, left, dd->comm, ctx->stream));
+    SCH_NCCL(ctx, n.Recv(base + (dd->Lloc + 2) * row, face, ncclDouble, right, dd->comm, ctx->stream));
+  }
+  SCH_NCCL(ctx, n.GroupEnd());
+  return SCH_OK;
+}
+
+// global sum of n partials (fixed order) into *out, then across ranks
+__global__ void k_dd_sum(const double* __restrict__ part, int n, double* __restrict__ out) {
+  __shared__ double slot[32];
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) acc += part[k];
+  double s = block_sum_rt(acc, slot);
+  if (threadIdx.x == 0) *out = s;
+}
+
+int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out) {
+  k_dd_sum<<<1, 256, 0, ctx->stream>>>(part, n, out);
+  SCH_LAUNCHED(ctx);
+  if (dd->comm != nullptr)
+    SCH_NCCL(ctx, nccl().AllReduce(out, out, 1, ncclDouble, ncclSum, dd->comm, ctx->stream));
+  return SCH_OK;
+}
+
+// ------------------------------------------------------------- CG state
+struct DDState {
+  double* sc;   // scalars: see SC_* below
+  int* flag;    // [S] need_x (X pass) per local strip (all equal)
+  double* beta; // [S] beta per local strip (all equal)
+  int* ctl;     // [0] done, [1] iters, [2] status
+};
+enum { SC_NORMB2 = 0, SC_PAP, SC_RR, SC_TN2, SC_RS, SC_RSNEW, SC_ALPHA, SC_NORMB, SC_TARGET,
+       SC_BEST, SC_RELRES, SC_COUNT };
+
+SCH_DEV bool own_row(long long i, int T, int Lext, int lo, int hi) {
+  const int row = (int)((i / T) % Lext);
+  return row >= lo && row < hi;
+}
+
+// x = x0|0 (all rows), r = p = b (all rows; b halos already exchanged),
+// partial ||b||^2 over own rows
+__global__ void k_dd_init(const double2* __restrict__ b, const double2* __restrict__ x0,
+                          double2* __restrict__ x, double2* __restrict__ r, double2* __restrict__ p,
+                          long long nsites, int T, int Lext, int lo, int hi, double* __restrict__ part) {
+  __shared__ double slot[32];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nsites;
+       i += (long long)gridDim.x * blockDim.x) {
+    Spinor bv = ld256_spinor_nc(b, i);
+    Spinor xv;
+    if (x0) xv = ld256_spinor_nc(x0, i);
+    else xv.s0 = xv.s1 = make_double2(0, 0);
+    st256_spinor(x, i, xv);
+    st256_spinor(r, i, bv);
+    st256_spinor(p, i, bv);
+    if (own_row(i, T, Lext, lo, hi)) acc += spinor_norm2(bv);
+  }
+  double s = block_sum_rt(acc, slot);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_dd_copy(const double2* __restrict__ src, double2* __restrict__ dst, long long nsites) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nsites;
+       i += (long long)gridDim.x * blockDim.x)
+    st256_spinor(dst, i, ld256_spinor(src, i));
+}
+
+__global__ void k_dd_ctrl_init(DDState st, int S, double tol, int have_x0) {
+  const double nb2 = st.sc[SC_NORMB2];
+  const double nb = sqrt(nb2);
+  st.sc[SC_NORMB] = nb;
+  st.sc[SC_TARGET] = tol * nb;
+  st.sc[SC_RS] = have_x0 ? st.sc[SC_RR] : nb2;
+  st.sc[SC_BEST] = INFINITY;
+  st.sc[SC_RELRES] = 0.0;
+  for (int s = 0; s < S; ++s) {
+    st.beta[s] = 0.0;
+    st.flag[s] = 0;
+  }
+  st.ctl[0] = nb == 0.0 ? 1 : 0;   // zero rhs: x = 0, 0 iterations (fermion.py:181-182)
+  st.ctl[1] = 0;
+  st.ctl[2] = 0;
+}
+
+__global__ void k_dd_alpha(DDState st) {
+  if (st.ctl[0]) return;
+  const double den = st.sc[SC_PAP];
+  st.sc[SC_ALPHA] = den > 0.0 ? st.sc[SC_RS] / den : 0.0;
+}
+
+// p = r + beta p, x += alpha p on every row; r -= alpha ap and ||r||^2 on own rows
+__global__ void k_dd_update(double2* __restrict__ r, double2* __restrict__ p, double2* __restrict__ x,
+                            const double2* __restrict__ ap, DDState st, long long nsites, int T, int Lext,
+                            int lo, int hi, int repl, double* __restrict__ part) {
+  __shared__ double slot[32];
+  if (st.ctl[0]) return;
+  const double al = st.sc[SC_ALPHA], be = st.beta[0];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nsites;
+       i += (long long)gridDim.x * blockDim.x) {
+    Spinor rv = ld256_spinor(r, i), pv = ld256_spinor(p, i), xv = ld256_spinor(x, i);
+    pv = sp_fma(be, pv, rv);
+    xv = sp_fma(al, pv, xv);
+    st256_spinor(p, i, pv);
+    st256_spinor(x, i, xv);
+    if (!repl && own_row(i, T, Lext, lo, hi)) {
+      rv = sp_fma(-al, ld256_spinor_nc(ap, i), rv);
+      st256_spinor(r, i, rv);
+      acc += spinor_norm2(rv);
+    }
+  }
+  double s = block_sum_rt(acc, slot);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_dd_check(DDState st, int S, int repl) {
+  if (st.ctl[0]) return;
+  int need;
+  if (repl) {
+    need = 1;
+  } else {
+    const double rsn = st.sc[SC_RR];
+    st.sc[SC_RSNEW] = rsn;
+    need = sqrt(rsn) <= st.sc[SC_TARGET];
+  }
+  for (int s = 0; s < S; ++s) st.flag[s] = need;
+}
+
+__global__ void k_dd_final(DDState st, int S, int it, int maxiter) {
+  if (st.ctl[0]) return;
+  const int nx = st.flag[0];
+  double rs_new = st.sc[SC_RSNEW];
+  if (nx) {
+    const double tn2 = st.sc[SC_TN2];
+    const double tn = sqrt(tn2);
+    const int repl = (it % kDDReplace) == 0;
+    if (!repl || tn <= st.sc[SC_TARGET]) st.sc[SC_BEST] = tn / st.sc[SC_NORMB];
+    if (tn <= st.sc[SC_TARGET]) {
+      st.ctl[0] = 1;
+      st.ctl[1] = it;
+      st.sc[SC_RELRES] = tn / st.sc[SC_NORMB];
+      for (int s = 0; s < S; ++s) st.flag[s] = 0;
+      return;
+    }
+    rs_new = tn2;
+  }
+  const double rs = st.sc[SC_RS];
+  const double beta = rs > 0.0 ? rs_new / rs : 0.0;
+  for (int s = 0; s < S; ++s) {
+    st.beta[s] = beta;
+    st.flag[s] = 0;
+  }
+  st.sc[SC_RS] = rs_new;
+  if (it >= maxiter) {
+    st.ctl[0] = 1;
+    st.ctl[1] = it;
+    st.ctl[2] = 1;
+    st.sc[SC_RELRES] = fmin(st.sc[SC_BEST], sqrt(rs_new) / st.sc[SC_NORMB]);
+  }
+}
+
+TileShape dd_tiles(int Lext, int T) { return pick_tile(Lext, T, false); }
+
+TileArgs dd_tile_args(sch_dd* dd, const TileShape& sh, const double2* U, double m0) {
+  TileArgs a{};
+  a.U = U;
+  a.B = dd->S;
+  a.L = dd->Lext;
+  a.T = dd->T;
+  a.tiles_t = sh.tiles_t;
+  a.tiles_per_chain = sh.tiles_x * sh.tiles_t;
+  a.diag = 2.0 + m0;
+  a.own_lo = kHalo;
+  a.own_hi = kHalo + dd->Lloc;
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sch_nccl_unique_id(sch_ctx* ctx, void* id_out) {
+  SCH_CHECK_ARG(ctx, id_out != nullptr, "nccl_unique_id: null output");
+  if (!nccl().ok) return sch_fail(ctx, SCH_ERR_CUDA, "libnccl.so.2 not available");
+  ncclUniqueId id;
+  SCH_NCCL(ctx, nccl().GetUniqueId(&id));
+  memcpy(id_out, id.internal, sizeof(id.internal));
+  return SCH_OK;
+}
+
+int sch_dd_create(sch_ctx* ctx, const void* nccl_id, int nranks, int rank, int L, int T,
+                  int strips_local, sch_dd** out) {
+  SCH_CHECK_ARG(ctx, out && nranks >= 1 && rank >= 0 && rank < nranks && strips_local >= 1,
+                "dd_create: bad ranks");
+  const int G = nranks * strips_local;
+  SCH_CHECK_ARG(ctx, L % G == 0 && L / G >= 2 && T >= 2, "dd_create: L must split into strips of >= 2 rows");
+  SCH_CHECK_ARG(ctx, nranks == 1 || strips_local == 1, "dd_create: NCCL transport holds one strip per rank");
+  sch_dd* dd = new sch_dd();
+  dd->nranks = nranks;
+  dd->rank = rank;
+  dd->S = strips_local;
+  dd->G = G;
+  dd->L = L;
+  dd->T = T;
+  dd->Lloc = L / G;
+  dd->Lext = dd->Lloc + 2 * kHalo;
+  if (nranks > 1) {
+    if (!nccl().ok) {
+      delete dd;
+      return sch_fail(ctx, SCH_ERR_CUDA, "libnccl.so.2 not available");
+    }
+    SCH_CHECK_ARG(ctx, nccl_id != nullptr, "dd_create: NCCL id required for nranks > 1");
+    ncclUniqueId id;
+    memcpy(id.internal, nccl_id, sizeof(id.internal));
+    ncclResult_t r = nccl().CommInitRank(&dd->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+      delete dd;
+      return sch_fail(ctx, SCH_ERR_CUDA, "ncclCommInitRank: %s", nccl().GetErrorString(r));
+    }
+  }
+  *out = dd;
+  return SCH_OK;
+}
+
+int sch_dd_destroy(sch_dd* dd) {
+  if (!dd) return SCH_OK;
+  if (dd->comm) nccl().CommDestroy(dd->comm);
+  delete dd;
+  return SCH_OK;
+}
+
+int sch_dd_geometry(const sch_dd* dd, int* out4) {
+  if (!dd || !out4) return SCH_ERR_ARG;
+  out4[0] = dd->S;
+  out4[1] = dd->Lloc;
+  out4[2] = dd->Lext;
+  out4[3] = dd->G;
+  return SCH_OK;
+}
+
+int sch_dd_exchange(sch_ctx* ctx, sch_dd* dd, double* field, int planes, int words_per_site) {
+  SCH_CHECK_ARG(ctx, dd && field && planes >= 1 && words_per_site >= 1, "dd_exchange: bad args");
+  return dd_exchange(ctx, dd, field, planes, words_per_site);
+}
+
+int sch_dd_ddagd(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* psi_ext, double* out_ext,
+                 double m0) {
+  SCH_CHECK_ARG(ctx, dd && U_ext && psi_ext && out_ext && psi_ext != out_ext, "dd_ddagd: bad args");
+  int rc = dd_exchange(ctx, dd, psi_ext, 1, 4);
+  if (rc) return rc;
+  TileShape sh = dd_tiles(dd->Lext, dd->T);
+  TileArgs a = dd_tile_args(dd, sh, (const double2*)U_ext, m0);
+  a.in = (const double2*)psi_ext;
+  a.out = (double2*)out_ext;
+  launch_normal_tile<MODE_PLAIN>(sh, a, ctx->stream);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ext, double* x_ext,
+                     double* x0_ext, double m0, double tol, int maxiter, int* h_iters,
+                     double* h_relres, int* h_status) {
+  SCH_CHECK_ARG(ctx, dd && U_ext && b_ext && x_ext && maxiter >= 1, "dd_cg_normal: bad args");
+  SCH_CHECK_ARG(ctx, x_ext != b_ext && x_ext != x0_ext, "dd_cg_normal: x aliases an input");
+  const TileShape sh = dd_tiles(dd->Lext, dd->T);
+  const int tpc = sh.tiles_x * sh.tiles_t;
+  const long long nsites = (long long)dd->S * dd->Lext * dd->T;
+  const size_t vec = (size_t)nsites * 2 * sizeof(double2);
+  const int ntile_part = dd->S * tpc;
+  const size_t bytes = 3 * vec + sizeof(double) * (2 * (size_t)std::max(ntile_part, kRedGrid) +
+                                                   SC_COUNT + dd->S + 64) +
+                       sizeof(int) * (dd->S + 8) + 8 * 256;
+  void* ws;
+  int rc = sch_workspace(ctx, bytes, &ws);
+  if (rc) return rc;
+  char* w = (char*)ws;
+  auto take = [&](size_t n) {
+    char* p = w;
+    w += (n + 255) & ~size_t(255);
+    return (void*)p;
+  };
+  double2* r = (double2*)take(vec);
+  double2* p = (double2*)take(vec);
+  double2* ap = (double2*)take(vec);
+  double* part_a = (double*)take(sizeof(double) * std::max(ntile_part, kRedGrid));
+  double* part_b = (double*)take(sizeof(double) * std::max(ntile_part, kRedGrid));
+  DDState st;
+  st.sc = (double*)take(sizeof(double) * SC_COUNT);
+  st.beta = (double*)take(sizeof(double) * dd->S);
+  st.flag = (int*)take(sizeof(int) * dd->S);
+  st.ctl = (int*)take(sizeof(int) * 8);
+  cudaStream_t s = ctx->stream;
+  const int lo = kHalo, hi = kHalo + dd->Lloc;
+  const unsigned egrid = kRedGrid;
+
+  // init: b (and x0) halos, then x, r, p on every row
+  if ((rc = dd_exchange(ctx, dd, b_ext, 1, 4))) return rc;
+  if (x0_ext && (rc = dd_exchange(ctx, dd, x0_ext, 1, 4))) return rc;
+  k_dd_init<<<egrid, 256, 0, s>>>((const double2*)b_ext, (const double2*)x0_ext, (double2*)x_ext, r, p,
+                                  nsites, dd->T, dd->Lext, lo, hi, part_a);
+  SCH_LAUNCHED(ctx);
+  if ((rc = dd_allsum(ctx, dd, part_a, egrid, st.sc + SC_NORMB2))) return rc;
+  TileArgs base = dd_tile_args(dd, sh, (const double2*)U_ext, m0);
+  if (x0_ext) {   // r = b - A x0 on own rows, then p = r, both with fresh halos
+    TileArgs tx = base;
+    tx.in = (const double2*)x_ext;
+    tx.bvec = (const double2*)b_ext;
+    tx.out = r;
+    tx.partial = part_b;
+    launch_normal_tile<MODE_X>(sh, tx, s);
+    SCH_LAUNCHED(ctx);
+    if ((rc = dd_allsum(ctx, dd, part_b, ntile_part, st.sc + SC_RR))) return rc;
+    if ((rc = dd_exchange(ctx, dd, (double*)r, 1, 4))) return rc;
+    k_dd_copy<<<egrid, 256, 0, s>>>(r, p, nsites);
+    SCH_LAUNCHED(ctx);
+  }
+  k_dd_ctrl_init<<<1, 1, 0, s>>>(st, dd->S, tol, x0_ext != nullptr);
+  SCH_LAUNCHED(ctx);
+
+  TileArgs tp = base;   // stencil pass: p = r + beta p formed on the fly
+  tp.in = r;
+  tp.in2 = p;
+  tp.out = ap;
+  tp.beta = st.beta;
+  tp.partial = part_a;
+  TileArgs txx = base;  // true residual / replacement pass
+  txx.in = (const double2*)x_ext;
+  txx.bvec = (const double2*)b_ext;
+  txx.out = r;
+  txx.flag = st.flag;
+  txx.partial = part_b;
+
+  int it = 1, chunk = 4;
+  while (it <= maxiter) {
+    const int n = std::min(chunk, maxiter - it + 1);
+    for (int j = 0; j < n; ++j, ++it) {
+      const int repl = (it % kDDReplace) == 0;
+      if ((rc = dd_exchange(ctx, dd, (double*)r, 1, 4))) return rc;
+      launch_normal_tile<MODE_P>(sh, tp, s);
+      SCH_LAUNCHED(ctx);
+      if ((rc = dd_allsum(ctx, dd, part_a, ntile_part, st.sc + SC_PAP))) return rc;
+      k_dd_alpha<<<1, 1, 0, s>>>(st);
+      SCH_LAUNCHED(ctx);
+      k_dd_update<<<egrid, 256, 0, s>>>(r, p, (double2*)x_ext, ap, st, nsites, dd->T, dd->Lext, lo,
+                                        hi, repl, part_b);
+      SCH_LAUNCHED(ctx);
+      if ((rc = dd_allsum(ctx, dd, part_b, egrid, st.sc + SC_RR))) return rc;
+      k_dd_check<<<1, 1, 0, s>>>(st, dd->S, repl);
+      SCH_LAUNCHED(ctx);
+      // x halos are current (x is updated on every row), so no exchange here
+      launch_normal_tile<MODE_X>(sh, txx, s);
+      SCH_LAUNCHED(ctx);
+      if ((rc = dd_allsum(ctx, dd, part_b, ntile_part, st.sc + SC_TN2))) return rc;
+      k_dd_final<<<1, 1, 0, s>>>(st, dd->S, it, maxiter);
+      SCH_LAUNCHED(ctx);
+    }
+    SCH_CUDA(ctx, cudaMemcpyAsync(ctx->h_flag, st.ctl, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SCH_CUDA(ctx, cudaStreamSynchronize(s));
+    if (*ctx->h_flag) break;
+    chunk = std::min(chunk * 2, 32);
+  }
+  int ctl[3];
+  double relres;
+  SCH_CUDA(ctx, cudaMemcpyAsync(ctl, st.ctl, sizeof(ctl), cudaMemcpyDeviceToHost, s));
+  SCH_CUDA(ctx, cudaMemcpyAsync(&relres, st.sc + SC_RELRES, sizeof(double), cudaMemcpyDeviceToHost, s));
+  SCH_CUDA(ctx, cudaStreamSynchronize(s));
+  if (ctl[1] == 0 && ctl[0]) {   // zero rhs: x = 0
+    SCH_CUDA(ctx, cudaMemsetAsync(x_ext, 0, vec, s));
+  }
+  if (h_iters) *h_iters = ctl[1];
+  if (h_relres) *h_relres = relres;
+  if (h_status) *h_status = ctl[2];
+  return ctl[2] ? sch_fail(ctx, SCH_ERR_SOLVER, "CG exceeded %d iterations", maxiter) : SCH_OK;
+}
+
+}  // extern "C"

@@ -42,6 +42,7 @@ struct TileArgs {
   int B, L, T;
   int tiles_t, tiles_per_chain;
   double diag;                      // 2 + m0
+  int own_lo, own_hi;               // x rows written / summed; own_hi == 0 => all rows
 };
 
 template <int TX, int TT, int HX, int HT, int MODE, int NT>
@@ -136,6 +137,7 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int c, int tile, do
     const int li = ri - HX, lj = rj - HT;
     if (li < 0 || li >= TX || lj < 0 || lj >= TT) continue;
     if (x0 + li >= L || t0 + lj >= T) continue;     // clipped tile
+    if (a.own_hi > 0 && (x0 + li < a.own_lo || x0 + li >= a.own_hi)) continue;   // DD halo row
     int kxp, kxm, ktp, ktm;
     nb(ri, rj, kxp, kxm, ktp, ktm);
     Spinor r = res_consume<true>(E, NR, t[j], u0[j], u1[j], kxp, kxm, ktp, ktm, a.diag);
@@ -227,7 +229,7 @@ inline TileShape pick_tile(int L, int T, bool tma = false) {
   if (L == 16 && T == 16) s = {0, 16, 16, 1, 1};
   else if (T == 32 && L % 16 == 0) s = {1, 16, 32, L / 16, 1};
   else if (T == 64 && L % 8 == 0) s = {2, 8, 64, L / 8, 1};
-  else if (T % 64 == 0 && L % 16 == 0 && T > 64) s = {3, 16, 64, L / 16, T / 64};
+  else if (T % 64 == 0 && T > 64) s = {3, 16, 64, (L + 15) / 16, T / 64};   // x-clipped
   else s = {4, 8, 16, (L + 7) / 8, (T + 15) / 16};
   return s;
 }

@@ -1,0 +1,78 @@
+"""Domain-decomposed D^dag D and CG (BASELINE configs[4]) against the
+single-lattice path and the oracle, with every strip on one GPU (local
+transport: the same CG loop, halo rows filled by a copy kernel instead of
+NCCL send/recv)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def npy(t):
+    return t.detach().cpu().numpy()
+
+
+@pytest.mark.parametrize("L,T,G", [(64, 32, 4), (32, 128, 2), (48, 16, 6), (16, 8, 8)])
+def test_dd_normal_and_cg_match_single_lattice(L, T, G):
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice
+    from oracle import schwinger_oracle as O
+    rng = np.random.default_rng(L + T + G)
+    q = rng.uniform(-np.pi, np.pi, (2, L, T))
+    psi = rng.standard_normal((L, T, 2)) + 1j * rng.standard_normal((L, T, 2))
+    lat = StripLattice(L, T, strips=G)
+    assert (lat.S, lat.Lloc, lat.Lext) == (G, L // G, L // G + 4)
+    op = DDWilsonDirac(lat, lat.scatter_links(q), 0.1)
+    ref = O.normal_op(O.fermion_links(q), psi, 0.1)
+    assert rel_err(npy(lat.gather_spinor(op.normal(lat.scatter_spinor(psi)))), ref) < 1e-12
+    x, it, rel = op.cg(lat.scatter_spinor(psi), 1e-10)
+    xo, ito, _ = O.cg_normal(O.fermion_links(q), 0.1, psi, 1e-10)
+    assert it == ito
+    assert rel <= 1e-10
+    assert rel_err(npy(lat.gather_spinor(x)), xo) < 1e-12
+    # the single-lattice GPU path agrees too
+    xs, its, _ = sw.cg_normal(sw.WilsonDirac(q, 0.1), psi, 1e-10)
+    assert its == it
+
+
+def test_dd_exchange_fills_halos_from_neighbours():
+    from paper_1512_03812_b200.dd import StripLattice
+    L, T, G = 24, 8, 3
+    lat = StripLattice(L, T, strips=G)
+    full = torch.arange(L * T * 4, dtype=torch.float64, device="cuda").reshape(L, T, 2, 2)
+    psi = torch.view_as_complex(full.contiguous())
+    ext = lat.scatter_spinor(psi)
+    want = ext.clone()
+    ext[:, :2] = 0
+    ext[:, -2:] = 0
+    lat.exchange(ext, 1, 4)
+    assert torch.equal(ext, want)
+
+
+def test_dd_cg_zero_rhs_warm_start_and_cap():
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice
+    L, T, G = 32, 16, 4
+    rng = np.random.default_rng(3)
+    q = 0.3 * rng.standard_normal((2, L, T))
+    lat = StripLattice(L, T, strips=G)
+    op = DDWilsonDirac(lat, lat.scatter_links(q), -0.231367)
+    zero = torch.zeros((G, L // G + 4, T, 2), dtype=torch.complex128, device="cuda")
+    x, it, _ = op.cg(zero, 1e-12)
+    assert it == 0 and torch.count_nonzero(x) == 0
+    b = rng.standard_normal((L, T, 2)) + 1j * rng.standard_normal((L, T, 2))
+    x0 = 0.1 * (rng.standard_normal((L, T, 2)) + 1j * rng.standard_normal((L, T, 2)))
+    x, it, rel = op.cg(lat.scatter_spinor(b), 1e-12, x0_ext=lat.scatter_spinor(x0))
+    from oracle import schwinger_oracle as O
+    xo, ito, _ = O.cg_normal(O.fermion_links(q), -0.231367, b, 1e-12, x0=x0)
+    # light mass, tol 1e-12, ~235 iterations: the strip-wise reduction order can
+    # move the stopping iteration by one; the solution still meets the rule
+    assert abs(it - ito) <= 1
+    assert rel <= 1e-12
+    assert rel_err(npy(lat.gather_spinor(x)), xo) < 1e-9
+    with pytest.raises(sw.SolverError):
+        op.cg(lat.scatter_spinor(b), 1e-12, maxiter=3)

@@ -57,6 +57,49 @@ def _worker(rank, world, port, total, out_q):
         dist.destroy_process_group()
 
 
+def _dd_worker(rank, world, port, L, T, out_q):
+    """Execute the NCCL face-exchange plan of csrc/dd.cu (dd.halo_plan) with
+    gloo point-to-point on CPU tensors and check every halo row."""
+    import torch
+    from paper_1512_03812_b200.dd import HALO, halo_plan
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lloc = L // world
+        full = torch.arange(L * T, dtype=torch.float64).reshape(L, T)
+        ext = torch.full((lloc + 2 * HALO, T), -1.0)
+        ext[HALO:HALO + lloc] = full[rank * lloc:(rank + 1) * lloc]
+        ops = []
+        for peer, row, n, kind in halo_plan(rank, world, lloc):
+            buf = ext[row:row + n]
+            if kind == "send":
+                ops.append(dist.P2POp(dist.isend, buf.contiguous(), peer))
+            else:
+                ops.append(dist.P2POp(dist.irecv, buf, peer))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        rows = (rank * lloc + np.arange(-HALO, lloc + HALO)) % L
+        out_q.put((rank, bool(torch.equal(ext, full[torch.as_tensor(rows)]))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dd_halo_plan_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_dd_worker, args=(r, world, port, 12, 5, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(res.values()), res
+
+
 @pytest.mark.parametrize("total", [7, 64])
 def test_gather_observables_world2_gloo(total):
     ctx = mp.get_context("spawn")
