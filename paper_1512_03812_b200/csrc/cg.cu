@@ -41,44 +41,54 @@ constexpr int kReplace = kResReplace;   // residual replacement period (fermion.
 // ============================================================ resident CG
 // (kernel in resident.cuh)
 
-template <int NT, int SPT, int MINB>
+template <int NT, int SPT, int MINB, int LC = 0, int TC = 0>
 int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
   const size_t smem = sizeof(double2) * 8 * (size_t)a.L * a.T;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cg_resident<NT, SPT, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(k_cg_resident<NT, SPT, MINB, LC, TC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  k_cg_resident<NT, SPT, MINB><<<B, NT, smem, ctx->stream>>>(a);
+  k_cg_resident<NT, SPT, MINB, LC, TC><<<B, NT, smem, ctx->stream>>>(a);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
 
 // Threads x sites-per-thread x min-CTAs-per-SM of the resident engine for V
-// sites.  SCH_RESIDENT ("NTxSPTxMINB", e.g. "128x2x4") overrides the default
-// for tuning runs.
+// sites; 16x16 and 32x32 get shape-specialised instantiations.
+// SCH_RESIDENT="NTxSPTxMINBxSPEC" overrides for tuning runs (SPEC 1 = use
+// the compile-time-shape kernel for this L x T, 0 = generic).
 int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
-  static int fnt = -1, fspt = 0, fminb = 0;
+  static int fnt = -1, fspt = 0, fminb = 0, fspec = 1;
   if (fnt < 0) {
     fnt = 0;
-    if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%dx%d", &fnt, &fspt, &fminb);
+    if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%dx%dx%d", &fnt, &fspt, &fminb, &fspec);
   }
   int nt, spt, minb;
-  if (fnt > 0 && (long long)fnt * fspt >= V) { nt = fnt; spt = fspt; minb = fminb; }
-  else if (V <= 128) { nt = 128; spt = 1; minb = 1; }
+  bool spec = true;
+  if (fnt > 0 && (long long)fnt * fspt >= V) {
+    nt = fnt; spt = fspt; minb = fminb; spec = fspec != 0;
+  } else if (V <= 128) { nt = 128; spt = 1; minb = 1; }
   else if (V <= 256) { nt = 128; spt = 2; minb = 4; }
   else if (V <= 512) { nt = 256; spt = 2; minb = 1; }
   else { nt = 256; spt = 4; minb = 1; }
+  const bool s16 = spec && a.L == 16 && a.T == 16 && (long long)nt * spt == 256;
+  const bool s32 = spec && a.L == 32 && a.T == 32 && (long long)nt * spt == 1024;
 #define SCH_RES(N, S, M) \
   if (nt == N && spt == S && minb == M) return launch_resident<N, S, M>(ctx, a, B);
-  SCH_RES(128, 1, 1) SCH_RES(128, 1, 6) SCH_RES(128, 1, 8)
-  SCH_RES(128, 2, 1) SCH_RES(128, 2, 4) SCH_RES(128, 2, 5) SCH_RES(128, 2, 6)
-  SCH_RES(256, 1, 1) SCH_RES(256, 1, 3) SCH_RES(256, 1, 4)
-  SCH_RES(256, 2, 1) SCH_RES(256, 2, 2) SCH_RES(256, 2, 3)
-  SCH_RES(256, 4, 1) SCH_RES(512, 2, 1) SCH_RES(512, 1, 1)
+#define SCH_RES16(N, S, M) \
+  if (s16 && nt == N && spt == S && minb == M) return launch_resident<N, S, M, 16, 16>(ctx, a, B);
+#define SCH_RES32(N, S, M) \
+  if (s32 && nt == N && spt == S && minb == M) return launch_resident<N, S, M, 32, 32>(ctx, a, B);
+  SCH_RES16(128, 2, 4) SCH_RES16(128, 2, 5) SCH_RES16(256, 1, 4) SCH_RES16(256, 1, 5)
+  SCH_RES32(256, 4, 1) SCH_RES32(512, 2, 1)
+  SCH_RES(128, 1, 1) SCH_RES(128, 2, 1) SCH_RES(128, 2, 4)
+  SCH_RES(256, 1, 4) SCH_RES(256, 2, 1) SCH_RES(256, 4, 1) SCH_RES(512, 2, 1)
 #undef SCH_RES
+#undef SCH_RES16
+#undef SCH_RES32
   return sch_fail(ctx, SCH_ERR_ARG, "no resident CG instantiation %dx%dx%d", nt, spt, minb);
 }
 

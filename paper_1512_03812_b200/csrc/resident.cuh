@@ -91,18 +91,39 @@ SCH_DEV Spinor sp_sub(const Spinor& a, const Spinor& b) {
   return r;
 }
 
-template <int NT, int SPT, int MINB>
+template <int NT, int SPT, int MINB, int LC = 0, int TC = 0>
 __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
   extern __shared__ double2 sm[];
   __shared__ double red[3][NT / 32];
-  const int L = a.L, T = a.T, V = L * T;
+  // LC/TC > 0: compile-time lattice (the hot 16^2 / 32^2 shapes): no guards,
+  // neighbour indices computed with shifts instead of held in registers
+  const int L = LC > 0 ? LC : a.L, T = TC > 0 ? TC : a.T, V = L * T;
+  static_assert(LC == 0 || LC * TC == NT * SPT, "specialised shape must fill the CTA");
   double2* E0 = sm;            // D-stage exports   [4][V]
   double2* E1 = sm + 4 * V;    // Ddag-stage exports [4][V]
   const int c = blockIdx.x;
   const long long cb = (long long)c * V;
   const int tid = threadIdx.x;
 
-  int site[SPT], nxp[SPT], nxm[SPT], ntp[SPT], ntm[SPT];
+  int site[SPT], nxp_[SPT], nxm_[SPT], ntp_[SPT], ntm_[SPT];
+  auto nbr = [&](int k, int which) -> int {
+    if constexpr (LC > 0) {
+      const int s = tid + k * NT;
+      const int xx = s / TC, tt = s % TC;
+      switch (which) {
+        case 0: return ((xx + 1) % LC) * TC + tt;
+        case 1: return ((xx + LC - 1) % LC) * TC + tt;
+        case 2: return xx * TC + (tt + 1) % TC;
+        default: return xx * TC + (tt + TC - 1) % TC;
+      }
+    } else {
+      return which == 0 ? nxp_[k] : which == 1 ? nxm_[k] : which == 2 ? ntp_[k] : ntm_[k];
+    }
+  };
+  auto valid = [&](int k) -> bool {
+    if constexpr (LC > 0) return true;
+    else return site[k] >= 0;
+  };
   double2 u0[SPT], u1[SPT];
   Spinor x[SPT], r[SPT], p[SPT];
   double bb = 0.0;
@@ -111,18 +132,20 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
     const int s = tid + k * NT;
     site[k] = s < V ? s : -1;
     x[k].s0 = x[k].s1 = make_double2(0, 0);
-    if (s < V) {
-      const int xx = s / T, tt = s - xx * T;
-      nxp[k] = (xx + 1 == L ? 0 : xx + 1) * T + tt;
-      nxm[k] = (xx == 0 ? L - 1 : xx - 1) * T + tt;
-      ntp[k] = xx * T + (tt + 1 == T ? 0 : tt + 1);
-      ntm[k] = xx * T + (tt == 0 ? T - 1 : tt - 1);
+    if (LC > 0 || s < V) {
+      if constexpr (LC == 0) {
+        const int xx = s / T, tt = s - xx * T;
+        nxp_[k] = (xx + 1 == L ? 0 : xx + 1) * T + tt;
+        nxm_[k] = (xx == 0 ? L - 1 : xx - 1) * T + tt;
+        ntp_[k] = xx * T + (tt + 1 == T ? 0 : tt + 1);
+        ntm_[k] = xx * T + (tt == 0 ? T - 1 : tt - 1);
+      }
       u0[k] = cscale(-0.5, __ldg(a.U + 2 * cb + s));        // exact: power-of-two scale
       u1[k] = cscale(-0.5, __ldg(a.U + 2 * cb + V + s));
       r[k] = ldg_spinor(a.b, cb + s);
       bb += spinor_norm2(r[k]);
     } else {
-      nxp[k] = nxm[k] = ntp[k] = ntm[k] = 0;
+      nxp_[k] = nxm_[k] = ntp_[k] = ntm_[k] = 0;
       u0[k] = u1[k] = make_double2(0, 0);
       r[k].s0 = r[k].s1 = make_double2(0, 0);
     }
@@ -133,7 +156,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
   if (normb == 0.0) {   // fermion.py:181-182, per chain
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
-      if (site[k] >= 0) st_spinor(a.x, cb + site[k], x[k]);
+      if (valid(k)) st_spinor(a.x, cb + site[k], x[k]);
     if (tid == 0) {
       a.iters[c] = 0;
       a.relres[c] = 0.0;
@@ -148,22 +171,22 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
   auto normal_op = [&](const Spinor* v, Spinor* out) {
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
-      if (site[k] >= 0) res_produce<false>(E0, V, site[k], v[k], u0[k], u1[k]);
+      if (valid(k)) res_produce<false>(E0, V, site[k], v[k], u0[k], u1[k]);
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
-      if (site[k] >= 0) {
-        Spinor t = res_consume<false, true>(E0, V, v[k], u0[k], u1[k], nxp[k], nxm[k], ntp[k],
-                                            ntm[k], a.diag);
+      if (valid(k)) {
+        Spinor t = res_consume<false, true>(E0, V, v[k], u0[k], u1[k], nbr(k, 0), nbr(k, 1),
+                                            nbr(k, 2), nbr(k, 3), a.diag);
         out[k] = t;
         res_produce<true>(E1, V, site[k], t, u0[k], u1[k]);
       }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
-      if (site[k] >= 0)
-        out[k] = res_consume<true, true>(E1, V, out[k], u0[k], u1[k], nxp[k], nxm[k], ntp[k],
-                                         ntm[k], a.diag);
+      if (valid(k))
+        out[k] = res_consume<true, true>(E1, V, out[k], u0[k], u1[k], nbr(k, 0), nbr(k, 1),
+                                         nbr(k, 2), nbr(k, 3), a.diag);
   };
 
   Spinor w[SPT];   // A applied to something
@@ -171,12 +194,12 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
   if (a.x0) {
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
-      if (site[k] >= 0) x[k] = ldg_spinor(a.x0, cb + site[k]);
+      if (valid(k)) x[k] = ldg_spinor(a.x0, cb + site[k]);
     normal_op(x, w);
     double rr = 0.0;
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
-      if (site[k] >= 0) {
+      if (valid(k)) {
         r[k] = sp_sub(r[k], w[k]);
         rr += spinor_norm2(r[k]);
       }
@@ -186,19 +209,44 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
   for (int k = 0; k < SPT; ++k) p[k] = r[k];
 
   double best = INFINITY;
+  constexpr int NW = NT / 32;
   for (int it = 1; it <= a.maxiter; ++it) {
-    normal_op(p, w);
-    double pap = 0.0;
+    // w = D^dag D p with <p, D^dag D p> formed as ||D p||^2 during the D stage:
+    // its warp partials are published by the barrier that already separates
+    // the D and D^dag stages, so the reduction costs no extra barrier and
+    // overlaps the D^dag stage.
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
-      if (site[k] >= 0) pap += spinor_redot(p[k], w[k]);
-    const double den = block_sum<NT>(pap, red[0]);
+      if (valid(k)) res_produce<false>(E0, V, site[k], p[k], u0[k], u1[k]);
+    __syncthreads();
+    double dd = 0.0;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k)
+      if (valid(k)) {
+        Spinor t = res_consume<false, true>(E0, V, p[k], u0[k], u1[k], nbr(k, 0), nbr(k, 1),
+                                            nbr(k, 2), nbr(k, 3), a.diag);
+        dd += spinor_norm2(t);
+        w[k] = t;
+        res_produce<true>(E1, V, site[k], t, u0[k], u1[k]);
+      }
+    dd = warp_sum(dd);
+    if ((tid & 31) == 0) red[0][tid >> 5] = dd;
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < SPT; ++k)
+      if (valid(k))
+        w[k] = res_consume<true, true>(E1, V, w[k], u0[k], u1[k], nbr(k, 0), nbr(k, 1), nbr(k, 2),
+                                       nbr(k, 3),
+                                       a.diag);
+    double den = 0.0;
+#pragma unroll
+    for (int q = 0; q < NW; ++q) den += red[0][q];
     const double alpha = den > 0.0 ? rs / den : 0.0;
     const bool repl = (it % kResReplace) == 0;
     double rsn = 0.0;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-      if (site[k] < 0) continue;
+      if (!valid(k)) continue;
       x[k] = sp_fma(alpha, p[k], x[k]);
       if (!repl) {
         r[k] = sp_fma(-alpha, w[k], r[k]);
@@ -216,7 +264,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
       double tn2 = 0.0;
 #pragma unroll
       for (int k = 0; k < SPT; ++k)
-        if (site[k] >= 0) {
+        if (valid(k)) {
           w[k] = sp_sub(ldg_spinor(a.b, cb + site[k]), w[k]);
           tn2 += spinor_norm2(w[k]);
         }
@@ -226,7 +274,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
       if (tn <= target) {
 #pragma unroll
         for (int k = 0; k < SPT; ++k)
-          if (site[k] >= 0) st_spinor(a.x, cb + site[k], x[k]);
+          if (valid(k)) st_spinor(a.x, cb + site[k], x[k]);
         if (tid == 0) {
           a.iters[c] = it;
           a.relres[c] = tn / normb;
@@ -245,7 +293,7 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
   }
 #pragma unroll
   for (int k = 0; k < SPT; ++k)
-    if (site[k] >= 0) st_spinor(a.x, cb + site[k], x[k]);
+    if (valid(k)) st_spinor(a.x, cb + site[k], x[k]);
   if (tid == 0) {
     a.iters[c] = a.maxiter;
     a.relres[c] = fmin(best, sqrt(rs) / normb);
