@@ -351,8 +351,10 @@ def run_ours(args):
     chains = shard.count
     cfg = sw.HmcConfig(h=1.0 / args.outer, **CFG3)
     geom = sw.LatticeGeom(cfg.L, cfg.T)
-    drng = sw.DeviceRng(seed=2024, stream0=shard.start)     # chain c <-> Philox key (seed, c)
-    q = sw.hot_start(sw.make_rng(2024, rank), geom, batch=chains)
+    # chain c draws exactly the reference's make_rng(2024, c) stream, on device:
+    # hot start first, then every trajectory's heatbaths and Metropolis draw
+    drng = sw.NumpyDeviceRng(seed=2024, n_chains=chains, stream0=shard.start)
+    q = drng.hot_start(geom)
 
     for _ in range(args.warmup):
         q, st = sw.hmc_update_ensemble(q, cfg, device_rng=drng)
@@ -436,7 +438,9 @@ def run_ours(args):
             "metric": "HMC trajectories/s", "value": value, "unit": "chain-trajectories/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64/c128", "data": "synthetic (hot start, device Philox heatbaths)",
+            "dtype": "f64/c128",
+            "data": "synthetic: hot start + heatbaths drawn on device from the reference's own "
+                    "streams (chain c == make_rng(2024, c), value-identical NumPy Philox/ziggurat)",
             "config": {"workload": f"{args.workload}: independent {cfg.L}x{cfg.T} chains, "
                                    f"beta={cfg.beta}, m0={cfg.m0}, tau={cfg.tau}, adapted-nested-fg "
                                    f"{args.outer}x{cfg.micro_per_call} steps (h={1.0 / args.outer}), "

@@ -147,6 +147,24 @@ int sch_rng_normal(sch_ctx* ctx, double* out, int B, long long per_chain, uint64
 int sch_rng_uniform(sch_ctx* ctx, double* out, int B, long long per_chain, uint64_t seed,
                     uint64_t stream0, uint64_t ctr);
 
+/* ---- bit-exact replica of the reference's NumPy streams ------------------
+ * np.random.Generator(np.random.Philox(key=[seed, stream0 + chain]))
+ * (lattice.py:86-104): one state per chain in device memory
+ * (sch_np_rng_state_bytes() bytes each); draws are value-identical to the
+ * host generator's (Philox4x64-10, NumPy's 256-layer ziggurat normal). */
+int sch_np_rng_state_bytes(void);
+int sch_np_rng_init(sch_ctx* ctx, void* state, int B, uint64_t seed, uint64_t stream0);
+/* mode 0: standard_normal, 1: uniform(lo, hi), 2: random(); out[b*n + i] */
+int sch_np_rng_fill(sch_ctx* ctx, void* state, double* out, int B, long long n_per_chain, int mode,
+                    double lo, double hi);
+/* hmc_update's heatbath draws per chain in the reference order
+ * (hmc.py:78-82, fermion.py:289): p[2V] normals, then phi = (re + i im) *
+ * phi_scale from 2V + 2V normals (phi unused when quenched) */
+int sch_np_heatbath(sch_ctx* ctx, void* state, double* p, double* phi, int B, long long V,
+                    double phi_scale, int quenched);
+/* metropolis (hmc.py:54-60): accept 1/0, -1 for non-finite dH; draws only if dH > 0 */
+int sch_np_metropolis(sch_ctx* ctx, void* state, const double* dh, int* accept, int B);
+
 /* ---- domain decomposition of one lattice (BASELINE configs[4]) -------- */
 /* One lattice split into G = nranks * strips_local x-strips of Lloc = L/G
  * rows.  Fields are "extended strips": [strips_local][Lloc+4][T] (2 halo

@@ -61,6 +61,11 @@ _SIGNATURES = {
     "sch_select_chains": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_int, _c_ll],
     "sch_metropolis": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_int],
     "sch_probe_fp64": [_c_ptr, _c_ptr, _c_int, _c_int],
+    "sch_np_rng_state_bytes": [],
+    "sch_np_rng_init": [_c_ptr, _c_ptr, _c_int, _c_u64, _c_u64],
+    "sch_np_rng_fill": [_c_ptr, _c_ptr, _c_ptr, _c_int, _c_ll, _c_int, _c_dbl, _c_dbl],
+    "sch_np_heatbath": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_int, _c_ll, _c_dbl, _c_int],
+    "sch_np_metropolis": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_int],
     "sch_nccl_unique_id": [_c_ptr, _c_ptr],
     "sch_dd_create": [_c_ptr, _c_ptr, _c_int, _c_int, _c_int, _c_int, _c_int,
                       ctypes.POINTER(_c_ptr)],

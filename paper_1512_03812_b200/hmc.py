@@ -24,7 +24,8 @@ from .config import HmcConfig
 from .fermion import InversionCounter, WilsonDirac, draw_phi, pseudofermion_heatbath, spinor_dot
 from .gauge import avg_plaquette, gauge_action
 from .integrators import IntegratorSpec, MdState, integrate_trajectory
-from .lattice import (DeviceRng, LatticeGeom, as_links, as_spinor, cold_start, kinetic_energy,
+from .lattice import (DeviceRng, LatticeGeom, NumpyDeviceRng, as_links, as_spinor, cold_start,
+                      kinetic_energy,
                       sample_momenta)
 
 log = logging.getLogger("schwinger")
@@ -208,6 +209,10 @@ def hmc_update_ensemble(q, config: HmcConfig, rngs=None, device_rng: DeviceRng |
                 phis.append(draw_phi(r, config.L, config.T))
         p = as_links(np.stack(ps))
         phi = as_spinor(np.stack(phis)) if phis else None
+    elif isinstance(device_rng, NumpyDeviceRng):   # the reference's streams, drawn on device
+        if device_rng.n != B:
+            raise ValueError(f"device streams for {device_rng.n} chains, links for {B}")
+        p, phi = device_rng.heatbath(geom, config.quenched)
     else:
         p = device_rng.normal(B, geom.links_shape())
         phi = None if config.quenched else device_rng.complex_normal(B, geom.spinor_shape(),
@@ -225,9 +230,12 @@ def hmc_update_ensemble(q, config: HmcConfig, rngs=None, device_rng: DeviceRng |
     h_end = hamiltonian(state)
     dh_dev = h_end - h_start
     if device_rng is not None:
-        u = device_rng.uniform(B)
-        acc = torch.empty((B,), dtype=torch.int32, device=q.device)
-        _lib.ctx().call("sch_metropolis", _lib.ptr(dh_dev), _lib.ptr(u), _lib.ptr(acc), B)
+        if isinstance(device_rng, NumpyDeviceRng):
+            acc = device_rng.metropolis(dh_dev)
+        else:
+            u = device_rng.uniform(B)
+            acc = torch.empty((B,), dtype=torch.int32, device=q.device)
+            _lib.ctx().call("sch_metropolis", _lib.ptr(dh_dev), _lib.ptr(u), _lib.ptr(acc), B)
         state.check_solves()
         dh = dh_dev.cpu().numpy()
         acc_h = acc.cpu().numpy()

@@ -186,6 +186,58 @@ class DeviceRng:
         return out
 
 
+class NumpyDeviceRng:
+    """Device replica of B reference streams: chain c draws exactly what
+    ``make_rng(seed, stream0 + c)`` would (lattice.py:86-89) — same Philox4x64
+    counter walk, same ziggurat normals, same uniform/random doubles — with the
+    state kept on the GPU.  Lets device-side ensembles (bench mode) keep
+    value-level parity with the reference's per-chain trajectories."""
+
+    def __init__(self, seed: int, n_chains: int, stream0: int = 0):
+        lib = _lib.load()
+        self.n = int(n_chains)
+        self.seed, self.stream0 = int(seed) % 2**64, int(stream0) % 2**64
+        nbytes = int(lib.sch_np_rng_state_bytes())
+        self.state = torch.empty((self.n * nbytes,), dtype=torch.uint8, device=device())
+        _lib.ctx().call("sch_np_rng_init", _lib.ptr(self.state), self.n, self.seed, self.stream0)
+
+    def _fill(self, shape, mode, lo=0.0, hi=0.0) -> torch.Tensor:
+        out = torch.empty((self.n,) + tuple(shape), dtype=torch.float64, device=device())
+        per = out.numel() // self.n
+        _lib.ctx().call("sch_np_rng_fill", _lib.ptr(self.state), _lib.ptr(out), self.n, per, mode,
+                        float(lo), float(hi))
+        return out
+
+    def standard_normal(self, shape) -> torch.Tensor:
+        return self._fill(shape, 0)
+
+    def uniform(self, low: float, high: float, shape) -> torch.Tensor:
+        return self._fill(shape, 1, low, high)
+
+    def random(self) -> torch.Tensor:
+        return self._fill((), 2).reshape(self.n)
+
+    def hot_start(self, geom: LatticeGeom) -> torch.Tensor:
+        """theta ~ U(-pi, pi) per chain (lattice.py:102-104)."""
+        return self.uniform(-np.pi, np.pi, geom.links_shape())
+
+    def heatbath(self, geom: LatticeGeom, quenched: bool = False):
+        """(p, phi) of hmc_update's draws, reference order (hmc.py:78-82)."""
+        p = torch.empty((self.n,) + geom.links_shape(), dtype=torch.float64, device=device())
+        phi = None if quenched else torch.empty((self.n,) + geom.spinor_shape(),
+                                                dtype=torch.complex128, device=device())
+        scale = 1.0 / np.sqrt(2.0)   # NumPy divides the complex phi by sqrt(2) this way
+        _lib.ctx().call("sch_np_heatbath", _lib.ptr(self.state), _lib.ptr(p), _lib.ptr(phi), self.n,
+                        geom.volume, float(scale), int(quenched))
+        return p, phi
+
+    def metropolis(self, dh: torch.Tensor) -> torch.Tensor:
+        """Accept flags (1/0, -1 for non-finite dH), one uniform iff dH > 0."""
+        acc = torch.empty((self.n,), dtype=torch.int32, device=dh.device)
+        _lib.ctx().call("sch_np_metropolis", _lib.ptr(self.state), _lib.ptr(dh), _lib.ptr(acc), self.n)
+        return acc
+
+
 # ---------------------------------------------------------------------------
 # elementary updates (device)
 # ---------------------------------------------------------------------------
