@@ -77,6 +77,32 @@ SCH_DEV Spinor res_consume(const double2* __restrict__ E, int V, const Spinor& v
   return r;
 }
 
+// consumer split in two: gather the four neighbour exports (issue all
+// shared-memory loads first), then combine
+struct Hops {
+  double2 f0, b0, f1, b1;
+};
+SCH_DEV Hops res_gather(const double2* __restrict__ E, int V, int nxp, int nxm, int ntp, int ntm) {
+  Hops h;
+  h.f0 = E[nxp];
+  h.b0 = E[V + nxm];
+  h.f1 = E[2 * V + ntp];
+  h.b1 = E[3 * V + ntm];
+  return h;
+}
+template <bool DAG>
+SCH_DEV Spinor res_combine(const Hops& h, const Spinor& v, double2 u0, double2 u1, double diag) {
+  const double2 hf0 = cmul(u0, h.f0);
+  const double2 hf1 = cmul(u1, h.f1);
+  double2 o0 = cadd(cadd(cadd(hf0, h.b0), hf1), h.b1);
+  double2 o1 = DAG ? cadd(csub(hf0, h.b0), cmuli(csub(hf1, h.b1)))
+                   : cadd(csub(h.b0, hf0), cmuli(csub(h.b1, hf1)));
+  Spinor r;   // links pre-scaled by -1/2
+  r.s0 = make_double2(__fma_rn(diag, v.s0.x, o0.x), __fma_rn(diag, v.s0.y, o0.y));
+  r.s1 = make_double2(__fma_rn(diag, v.s1.x, o1.x), __fma_rn(diag, v.s1.y, o1.y));
+  return r;
+}
+
 SCH_DEV Spinor sp_fma(double a, const Spinor& p, const Spinor& x) {   // a*p + x
   Spinor r;
   r.s0 = make_double2(__fma_rn(a, p.s0.x, x.s0.x), __fma_rn(a, p.s0.y, x.s0.y));
@@ -220,11 +246,14 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
       if (valid(k)) res_produce<false>(E0, V, site[k], p[k], u0[k], u1[k]);
     __syncthreads();
     double dd = 0.0;
+    Hops hp[SPT];
+#pragma unroll
+    for (int k = 0; k < SPT; ++k)   // all neighbour loads in flight before any math
+      if (valid(k)) hp[k] = res_gather(E0, V, nbr(k, 0), nbr(k, 1), nbr(k, 2), nbr(k, 3));
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
       if (valid(k)) {
-        Spinor t = res_consume<false, true>(E0, V, p[k], u0[k], u1[k], nbr(k, 0), nbr(k, 1),
-                                            nbr(k, 2), nbr(k, 3), a.diag);
+        Spinor t = res_combine<false>(hp[k], p[k], u0[k], u1[k], a.diag);
         dd += spinor_norm2(t);
         w[k] = t;
         res_produce<true>(E1, V, site[k], t, u0[k], u1[k]);
@@ -234,10 +263,10 @@ __global__ void __launch_bounds__(NT, MINB) k_cg_resident(ResArgs a) {
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < SPT; ++k)
-      if (valid(k))
-        w[k] = res_consume<true, true>(E1, V, w[k], u0[k], u1[k], nbr(k, 0), nbr(k, 1), nbr(k, 2),
-                                       nbr(k, 3),
-                                       a.diag);
+      if (valid(k)) hp[k] = res_gather(E1, V, nbr(k, 0), nbr(k, 1), nbr(k, 2), nbr(k, 3));
+#pragma unroll
+    for (int k = 0; k < SPT; ++k)
+      if (valid(k)) w[k] = res_combine<true>(hp[k], w[k], u0[k], u1[k], a.diag);
     double den = 0.0;
 #pragma unroll
     for (int q = 0; q < NW; ++q) den += red[0][q];
