@@ -540,6 +540,24 @@ def run_cfg5(args):
         t = torch.tensor([ms, cg_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, cg_ms = float(t[0]), float(t[1])
+    # one full trajectory of the configs[4] schedule on the strips
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200.dd_hmc import dd_hmc_update
+    w = WORKLOADS["cfg5"]["phys"]
+    cfg = sw.HmcConfig(L=L, T=T, beta=w["beta"], m0=w["m0"], tau=w["tau"], h=w["tau"] / args.outer,
+                       scheme=w["scheme"], micro_per_call=w["micro_per_call"], cg_tol=w["cg_tol"])
+    q_ext = lat.scatter_links(np.random.default_rng(5).uniform(-np.pi, np.pi, (2, L, T)))
+    sync()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0.record()
+    q_ext, traj = dd_hmc_update(lat, q_ext, cfg, sw.make_rng(5, 0))
+    g1.record()
+    sync()
+    traj_ms = g0.elapsed_time(g1)
+    if world > 1:
+        t = torch.tensor([traj_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        traj_ms = float(t[0])
     sites = L * T
     gbs = 96.0 * sites / (ms * 1e-3) / 1e9
     cg_gbs = 352.0 * sites * iters / (cg_ms * 1e-3) / 1e9
@@ -556,7 +574,13 @@ def run_cfg5(args):
                          "unit": "GB/s per GPU", "frac": gbs / max(world, 1) / hbm_peak,
                          "peak_kind": peak_kind},
             "cg": {"iterations": iters, "ms": cg_ms, "ms_per_iteration": cg_ms / max(iters, 1),
-                   "effective_GBs": cg_gbs, "rel_residual": rel}}), flush=True)
+                   "effective_GBs": cg_gbs, "rel_residual": rel},
+            "trajectory": {"scheme": cfg.scheme, "outer": args.outer,
+                           "micro_per_call": cfg.micro_per_call, "tau": cfg.tau,
+                           "ms": traj_ms, "trajectories_per_s": 1e3 / traj_ms, "dh": traj.dh,
+                           "inversions": traj.inversions,
+                           "includes": "host heatbath draws of the full lattice (reference "
+                                       "generator), H at both ends, Metropolis"}}), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

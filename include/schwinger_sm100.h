@@ -181,6 +181,10 @@ int sch_dd_destroy(sch_dd* dd);
 int sch_dd_geometry(const sch_dd* dd, int* out4);
 /* refresh the halo rows of a field [S][planes][Lext][T][words_per_site] (doubles) */
 int sch_dd_exchange(sch_ctx* ctx, sch_dd* dd, double* field, int planes, int words_per_site);
+/* out[s] = per-strip sum over the own rows: kind 0 = 0.5*sum p^2 (momenta),
+ * 1 = sum(1 - cos theta) (links), 2 = Re sum conj(a) b (spinors a, b) */
+int sch_dd_own_sum(sch_ctx* ctx, sch_dd* dd, int kind, const double* a, const double* b,
+                   double* out);
 /* out = D^dag D psi on the own rows (psi's halos are refreshed first);
  * WilsonDirac.normal (fermion.py:129-131) on a decomposed lattice */
 int sch_dd_ddagd(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* psi_ext, double* out_ext,

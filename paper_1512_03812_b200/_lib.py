@@ -72,6 +72,7 @@ _SIGNATURES = {
     "sch_dd_destroy": [_c_ptr],
     "sch_dd_geometry": [_c_ptr, ctypes.POINTER(_c_int)],
     "sch_dd_exchange": [_c_ptr, _c_ptr, _c_ptr, _c_int, _c_int],
+    "sch_dd_own_sum": [_c_ptr, _c_ptr, _c_int, _c_ptr, _c_ptr, _c_ptr],
     "sch_dd_ddagd": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_dbl],
     "sch_dd_cg_normal": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_dbl, _c_dbl, _c_int,
                          ctypes.POINTER(_c_int), ctypes.POINTER(_c_dbl), ctypes.POINTER(_c_int)],

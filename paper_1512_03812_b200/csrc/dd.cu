@@ -317,6 +317,51 @@ __global__ void k_dd_final(DDState st, int S, int it, int maxiter) {
 
 TileShape dd_tiles(int Lext, int T) { return pick_tile(Lext, T, false); }
 
+// own-row sums, one CTA column per strip, fixed grid => deterministic
+__global__ void k_dd_own_sum(int kind, const double* __restrict__ a, const double* __restrict__ b,
+                             int Lext, int T, int lo, int hi, double* __restrict__ part) {
+  __shared__ double slot[32];
+  const int s = blockIdx.y;
+  const long long plane = (long long)Lext * T;
+  const long long own = (long long)(hi - lo) * T;
+  double acc = 0.0;
+  if (kind == 0) {
+    const double* ps = a + (long long)s * 2 * plane;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 2 * own;
+         i += (long long)gridDim.x * blockDim.x) {
+      const long long mu = i / own, k = i - mu * own;
+      const double v = ps[mu * plane + lo * (long long)T + k];
+      acc += v * v;
+    }
+  } else if (kind == 1) {
+    const double* qs = a + (long long)s * 2 * plane;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < own;
+         i += (long long)gridDim.x * blockDim.x) {
+      const int x = lo + (int)(i / T), t = (int)(i % T);
+      acc += 1.0 - cos(plaq(qs, Lext, T, x, t));
+    }
+  } else {
+    const double2* as = (const double2*)a + (long long)s * 2 * plane;
+    const double2* bs = (const double2*)b + (long long)s * 2 * plane;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 2 * own;
+         i += (long long)gridDim.x * blockDim.x) {
+      const long long e = 2 * lo * (long long)T + i;
+      acc += redot(as[e], bs[e]);
+    }
+  }
+  const double v = block_sum_rt(acc, slot);
+  if (threadIdx.x == 0) part[(long long)s * gridDim.x + blockIdx.x] = v;
+}
+
+__global__ void k_dd_strip_finish(const double* __restrict__ part, int S, int kind,
+                                  double* __restrict__ out) {
+  for (int s = threadIdx.x; s < S; s += blockDim.x) {
+    double v = 0.0;
+    for (int k = 0; k < kRedGrid; ++k) v += part[(long long)s * kRedGrid + k];
+    out[s] = kind == 0 ? 0.5 * v : v;
+  }
+}
+
 TileArgs dd_tile_args(sch_dd* dd, const TileShape& sh, const double2* U, double m0) {
   TileArgs a{};
   a.U = U;
@@ -391,6 +436,26 @@ int sch_dd_geometry(const sch_dd* dd, int* out4) {
   out4[1] = dd->Lloc;
   out4[2] = dd->Lext;
   out4[3] = dd->G;
+  return SCH_OK;
+}
+
+// Per-strip sums over the own rows of extended fields (the Hamiltonian's
+// reductions on a decomposed lattice):
+//   kind 0: 0.5 * sum a^2            a = momenta [S][2][Lext][T]      (lattice.py:128-130)
+//   kind 1: sum (1 - cos theta)      a = links   [S][2][Lext][T]      (gauge.py:37-40)
+//   kind 2: Re sum conj(a) b         a, b = spinors [S][Lext][T][2]   (fermion.py:54-56)
+int sch_dd_own_sum(sch_ctx* ctx, sch_dd* dd, int kind, const double* a, const double* b,
+                   double* out) {
+  SCH_CHECK_ARG(ctx, dd && a && out && kind >= 0 && kind <= 2 && (kind != 2 || b),
+                "dd_own_sum: bad args");
+  void* ws;
+  int rc = sch_workspace(ctx, sizeof(double) * (size_t)dd->S * kRedGrid, &ws);
+  if (rc) return rc;
+  k_dd_own_sum<<<dim3(kRedGrid, dd->S), 256, 0, ctx->stream>>>(kind, a, b, dd->Lext, dd->T, kHalo,
+                                                               kHalo + dd->Lloc, (double*)ws);
+  SCH_LAUNCHED(ctx);
+  k_dd_strip_finish<<<1, 64, 0, ctx->stream>>>((const double*)ws, dd->S, kind, out);
+  SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
 

@@ -101,6 +101,10 @@ class StripLattice:
         """Own rows of an extended field along the x axis ``axis``."""
         return ext.narrow(axis, HALO, self.Lloc)
 
+    def gather_links(self, ext) -> torch.Tensor:
+        """(S, 2, Lext, T) -> own rows (2, S*Lloc, T) in global row order."""
+        return torch.cat([ext[s][:, HALO:HALO + self.Lloc] for s in range(self.S)], dim=1)
+
     def gather_spinor(self, ext) -> torch.Tensor:
         """Local strips' own rows, concatenated in global row order."""
         return torch.cat([self.own(ext[s], 0) for s in range(self.S)], dim=0)

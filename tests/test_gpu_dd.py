@@ -39,6 +39,34 @@ def test_dd_normal_and_cg_match_single_lattice(L, T, G):
     assert its == it
 
 
+@pytest.mark.parametrize("scheme,h,G", [("adapted-nested-fg", 0.25, 4), ("5stage", 0.2, 2),
+                                        ("nested-leapfrog", 0.25, 8)])
+def test_dd_hmc_update_matches_reference_full_lattice(scheme, h, G):
+    """HMC on strips (draws from the full-lattice reference generator) ==
+    the oracle's hmc_update on the whole lattice: dH <= 1e-8, same accept
+    sequence and inversion count, same final links."""
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200.dd import StripLattice
+    from paper_1512_03812_b200.dd_hmc import dd_hmc_update
+    from oracle import schwinger_oracle as O
+    L = 16
+    kw = dict(L=L, T=L, beta=2.0, m0=0.1, tau=1.0 if scheme != "5stage" else 0.4, h=h,
+              scheme=scheme, micro_per_call=2 if scheme.startswith(("nested", "adapted")) else None,
+              cg_tol=1e-10)
+    cfg, ocfg = sw.HmcConfig(**kw), O.Config(**kw)
+    lat = StripLattice(L, L, strips=G)
+    rng_g, rng_o = O.make_rng(4, 0), O.make_rng(4, 0)
+    q0 = O.hot_start(rng_g, L, L)
+    assert np.array_equal(q0, O.hot_start(rng_o, L, L))
+    q_ext, qo = lat.scatter_links(q0), q0
+    for _ in range(2):
+        q_ext, s = dd_hmc_update(lat, q_ext, cfg, rng_g)
+        qo, so = O.hmc_update(qo, ocfg, rng_o)
+        assert abs(s.dh - so["dh"]) < 1e-8
+        assert s.accepted == so["accepted"] and s.inversions == so["inversions"]
+    assert np.max(np.abs(npy(lat.gather_links(q_ext)) - qo)) < 1e-8
+
+
 def test_dd_exchange_fills_halos_from_neighbours():
     from paper_1512_03812_b200.dd import StripLattice
     L, T, G = 24, 8, 3
