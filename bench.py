@@ -292,7 +292,7 @@ def stencil_bench(torch, sw, _lib, hbm_peak):
            "ddagd": {"achieved": ddd_gbs, "peak": hbm_peak, "unit": "GB/s",
                      "frac": ddd_gbs / hbm_peak, "us_per_application": t * 1e6,
                      "bytes_model": "96 B/site (psi in + U + out)",
-                     "kernel": "k_normal_tma<8,32,PLAIN,256 thr,2 stages,3 CTA/SM> "
+                     "kernel": "k_normal_tma<8,32,PLAIN,128 thr,2 stages,3 CTA/SM> "
                                "(persistent, cp.async.bulk + mbarrier pipeline)"}}
     # CG, both engines (an untimed short solve first loads every kernel)
     for mode, label in (("per_chain", "resident"), ("batch_global", "streaming")):

@@ -236,7 +236,7 @@ inline int tma_cfg() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SCH_TMA_CFG");
-    v = e ? atoi(e) : 2;   // measured best on cfg2 (profiles/r01/README.md)
+    v = e ? atoi(e) : 6;   // measured best on cfg2 (profiles/r01/README.md)
   }
   return v;
 }
@@ -244,9 +244,9 @@ inline int tma_cfg() {
 // Host: shapes handled by the TMA path (whole time rows, x tiles of TX rows).
 inline bool tma_tile_shape(int L, int T, int& TX) {
   if (T == 32) {
-    static const int tx_of_cfg[] = {8, 16, 8, 4, 8};
+    static const int tx_of_cfg[] = {8, 16, 8, 4, 8, 8, 8};
     const int c = tma_cfg();
-    TX = tx_of_cfg[(c >= 0 && c < 5) ? c : 0];
+    TX = tx_of_cfg[(c >= 0 && c < 7) ? c : 0];
     return L % TX == 0;
   }
   if (T == 16 && L % 16 == 0) { TX = 16; return true; }
@@ -286,6 +286,8 @@ inline bool launch_normal_tma(const TileArgs& a, cudaStream_t st, int num_sms) {
       case 2: launch_tma_inst<8, 32, MODE, 256, 2, 3>(a, st, num_sms); break;
       case 3: launch_tma_inst<4, 32, MODE, 256, S, 3>(a, st, num_sms); break;
       case 4: launch_tma_inst<8, 32, MODE, 384, 2, 2>(a, st, num_sms); break;
+      case 5: launch_tma_inst<8, 32, MODE, 192, 2, 3>(a, st, num_sms); break;
+      case 6: launch_tma_inst<8, 32, MODE, 128, 2, 3>(a, st, num_sms); break;
       default: launch_tma_inst<8, 32, MODE, 384, S, 2>(a, st, num_sms); break;
     }
   } else if (a.T == 16) {
