@@ -32,6 +32,7 @@ int sch_ctx_destroy(sch_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   else cudaDeviceSynchronize();
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   if (c->ws) cudaFree(c->ws);
   if (c->h_flag) cudaFreeHost(c->h_flag);
   delete c;

@@ -104,6 +104,8 @@ struct StreamState {
   // global
   int* n_active;   // chains still iterating; 0 => done
   int* n_active_init;
+  int* it;         // current iteration (1-based), advanced on the device
+                   // so a captured chunk of iterations can be replayed
   // partials [B][tpc]
   double *part_pap, *part_rr, *part_rr2, *part_bb;
   int B, tpc, global_mode;
@@ -168,8 +170,9 @@ __global__ void k_copy_r_to_p(ElemArgs e) {
 // With few tiles per chain (FUSE_ALPHA) every thread forms alpha itself from
 // the chain's <p,Ap> tile partials, in the same fixed order as k_ctrl_alpha.
 template <bool FUSE_ALPHA>
-__global__ void k_cg_update(ElemArgs e, StreamState st, int repl) {
+__global__ void k_cg_update(ElemArgs e, StreamState st) {
   __shared__ double slot[32];
+  const int repl = (*st.it % kReplace) == 0;
   const int c = blockIdx.x / e.tpc, tile = blockIdx.x - c * e.tpc;
   if (!st.active[c]) return;
   double al;
@@ -270,6 +273,7 @@ __global__ void k_ctrl_init_global(StreamState st) {
     if (st.normb[c] != 0.0) atomicAdd(&nz, 1);
   }
   __syncthreads();
+  if (threadIdx.x == 0) *st.it = 1;
   if (st.global_mode && nz == 0) {
     for (int c = threadIdx.x; c < st.B; c += blockDim.x) st.active[c] = 0;
     if (threadIdx.x == 0) *st.n_active = *st.n_active_init = 0;
@@ -290,8 +294,9 @@ __global__ void k_ctrl_alpha(StreamState st) {
 
 // after the update: rs' and the convergence check
 template <bool PT>
-__global__ void k_ctrl_check(StreamState st, int repl) {
+__global__ void k_ctrl_check(StreamState st) {
   __shared__ double slot[32];
+  const int repl = (*st.it % kReplace) == 0;
   const int c = ctrl_chain<PT>();
   if (c >= st.B || !st.active[c]) return;
   if (repl) {
@@ -311,7 +316,8 @@ __global__ void k_ctrl_check(StreamState st, int repl) {
 }
 
 // global mode: the true-residual branch runs only when every chain passes
-__global__ void k_ctrl_check_global(StreamState st, int repl) {
+__global__ void k_ctrl_check_global(StreamState st) {
+  const int repl = (*st.it % kReplace) == 0;
   __shared__ int fails;
   if (threadIdx.x == 0) fails = 0;
   __syncthreads();
@@ -326,8 +332,9 @@ __global__ void k_ctrl_check_global(StreamState st, int repl) {
 
 // after the (optional) true-residual pass
 template <bool PT>
-__global__ void k_ctrl_final(StreamState st, int it) {
+__global__ void k_ctrl_final(StreamState st) {
   __shared__ double slot[32];
+  const int it = *st.it;
   const int c = ctrl_chain<PT>();
   if (c >= st.B || !st.active[c]) return;
   const int nx = st.need_x[c];
@@ -361,7 +368,8 @@ __global__ void k_ctrl_final(StreamState st, int it) {
   }
 }
 
-__global__ void k_ctrl_final_global(StreamState st, int it) {
+__global__ void k_ctrl_final_global(StreamState st) {
+  const int it = *st.it;
   __shared__ int fails, any_x;
   __shared__ double worst;
   if (threadIdx.x == 0) {
@@ -409,6 +417,10 @@ __global__ void k_ctrl_final_global(StreamState st, int it) {
   }
   __syncthreads();
   if (threadIdx.x == 0 && (converged || it >= st.maxiter)) *st.n_active = 0;
+}
+
+__global__ void k_iter_inc(StreamState st) {
+  if (threadIdx.x == 0) ++*st.it;
 }
 
 // Chains whose rhs is exactly zero return x = 0 (fermion.py:181-182): per
@@ -462,6 +474,7 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
   st.pass = (int*)take(B * 4);
   st.n_active = (int*)take(4);
   st.n_active_init = (int*)take(4);
+  st.it = (int*)take(4);
   st.part_pap = (double*)take((size_t)B * tpc * 8);
   st.part_rr = (double*)take((size_t)B * tpc * 8);
   st.part_rr2 = (double*)take((size_t)B * tpc * 8);
@@ -531,46 +544,84 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
   txx.flag = st.need_x;
   txx.partial = st.part_rr2;
 
-  int it = 1;
-  int chunk = 4;
-  while (it <= maxiter) {
-    int n = std::min(chunk, maxiter - it + 1);
-    for (int j = 0; j < n; ++j, ++it) {
-      const int repl = (it % kReplace) == 0;
-      if (tma_p) launch_normal_tma<MODE_P>(tp, s, ctx->num_sms);
-      else launch_normal_tile<MODE_P>(sh, tp, s);
-      SCH_LAUNCHED(ctx);
-      if (pt) {
-        k_cg_update<true><<<ngrid, 256, 0, s>>>(e, st, repl);
-        SCH_LAUNCHED(ctx);
-        k_ctrl_check<true><<<cgrid, 128, 0, s>>>(st, repl);
-        SCH_LAUNCHED(ctx);
-      } else {
-        k_ctrl_alpha<false><<<cgrid, 128, 0, s>>>(st);
-        SCH_LAUNCHED(ctx);
-        k_cg_update<false><<<ngrid, 256, 0, s>>>(e, st, repl);
-        SCH_LAUNCHED(ctx);
-        k_ctrl_check<false><<<cgrid, 128, 0, s>>>(st, repl);
-        SCH_LAUNCHED(ctx);
-      }
-      if (global_mode) {
-        k_ctrl_check_global<<<1, 1024, 0, s>>>(st, repl);
-        SCH_LAUNCHED(ctx);
-      }
-      launch_normal_tile<MODE_X>(sh, txx, s, sparse);
-      SCH_LAUNCHED(ctx);
-      if (pt) k_ctrl_final<true><<<cgrid, 128, 0, s>>>(st, it);
-      else k_ctrl_final<false><<<cgrid, 128, 0, s>>>(st, it);
-      SCH_LAUNCHED(ctx);
-      if (global_mode) {
-        k_ctrl_final_global<<<1, 1024, 0, s>>>(st, it);
-        SCH_LAUNCHED(ctx);
-      }
+  // One CG iteration; every decision (replacement, convergence, maxiter)
+  // is made on the device from st.it, so the sequence can be captured once
+  // and replayed.  Returns the number of kernels enqueued.
+  auto enqueue_iteration = [&](cudaStream_t q) -> int {
+    int n = 0;
+    if (tma_p) launch_normal_tma<MODE_P>(tp, q, ctx->num_sms);
+    else launch_normal_tile<MODE_P>(sh, tp, q);
+    ++n;
+    if (pt) {
+      k_cg_update<true><<<ngrid, 256, 0, q>>>(e, st);
+      k_ctrl_check<true><<<cgrid, 128, 0, q>>>(st);
+      n += 2;
+    } else {
+      k_ctrl_alpha<false><<<cgrid, 128, 0, q>>>(st);
+      k_cg_update<false><<<ngrid, 256, 0, q>>>(e, st);
+      k_ctrl_check<false><<<cgrid, 128, 0, q>>>(st);
+      n += 3;
     }
+    if (global_mode) {
+      k_ctrl_check_global<<<1, 1024, 0, q>>>(st);
+      ++n;
+    }
+    launch_normal_tile<MODE_X>(sh, txx, q, sparse);
+    ++n;
+    if (pt) k_ctrl_final<true><<<cgrid, 128, 0, q>>>(st);
+    else k_ctrl_final<false><<<cgrid, 128, 0, q>>>(st);
+    ++n;
+    if (global_mode) {
+      k_ctrl_final_global<<<1, 1024, 0, q>>>(st);
+      ++n;
+    }
+    k_iter_inc<<<1, 32, 0, q>>>(st);
+    return n + 1;
+  };
+  auto poll_done = [&]() -> int {
     SCH_CUDA(ctx, cudaMemcpyAsync(ctx->h_flag, st.n_active, sizeof(int), cudaMemcpyDeviceToHost, s));
     SCH_CUDA(ctx, cudaStreamSynchronize(s));
-    if (*ctx->h_flag == 0) break;
-    chunk = std::min(chunk * 2, 32);
+    return *ctx->h_flag == 0 ? 1 : 0;
+  };
+
+  if (use_cg_graph()) {
+    // capture kChunk iterations once on a private stream, replay on s
+    constexpr int kChunk = 8;
+    if (!ctx->cap_stream)
+      SCH_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    SCH_CUDA(ctx, cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
+    int per = 0;
+    for (int j = 0; j < kChunk; ++j) per += enqueue_iteration(ctx->cap_stream);
+    cudaError_t ce = cudaGetLastError();
+    SCH_CUDA(ctx, cudaStreamEndCapture(ctx->cap_stream, &graph));
+    if (ce != cudaSuccess)
+      return sch_fail(ctx, SCH_ERR_CUDA, "cg capture: %s", cudaGetErrorString(ce));
+    cudaGraphExec_t exec;
+    SCH_CUDA(ctx, cudaGraphInstantiate(&exec, graph, 0));
+    cudaGraphDestroy(graph);
+    const int max_chunks = maxiter / kChunk + 2;
+    int rc2 = SCH_OK;
+    for (int k = 0; k < max_chunks; ++k) {
+      cudaError_t le = cudaGraphLaunch(exec, s);
+      if (le != cudaSuccess) {
+        rc2 = sch_fail(ctx, SCH_ERR_CUDA, "cg graph launch: %s", cudaGetErrorString(le));
+        break;
+      }
+      ctx->launches += per;
+      if (poll_done()) break;
+    }
+    cudaGraphExecDestroy(exec);
+    if (rc2) return rc2;
+  } else {
+    int done_iters = 0, chunk = 4;
+    while (done_iters < maxiter + 1) {
+      for (int j = 0; j < chunk; ++j) ctx->launches += enqueue_iteration(s);
+      SCH_LAUNCHED(ctx);
+      done_iters += chunk;
+      if (poll_done()) break;
+      chunk = std::min(chunk * 2, 32);
+    }
   }
   k_zero_x_if_null<<<ngrid, 256, 0, s>>>(e, st);
   SCH_LAUNCHED(ctx);

@@ -22,6 +22,9 @@ struct sch_ctx {
   size_t ws_bytes = 0;
   // pinned host scalar for streaming-CG termination polls
   int* h_flag = nullptr;
+  // private non-blocking stream for CUDA-graph capture (the caller's stream
+  // may be the legacy default stream, which cannot be captured)
+  cudaStream_t cap_stream = nullptr;
   // CUDA-graph cache for the streaming CG chunk
   struct GraphEntry {
     std::vector<long long> key;
@@ -99,6 +102,17 @@ inline bool use_tma() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SCH_NO_TMA");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// The streaming CG replays captured chunks of iterations as a CUDA graph;
+// SCH_NO_CG_GRAPH=1 launches every kernel from the host instead.
+inline bool use_cg_graph() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCH_NO_CG_GRAPH");
     v = (e && e[0] == '1') ? 0 : 1;
   }
   return v == 1;
