@@ -277,8 +277,10 @@ def stencil_bench(torch, sw, _lib, hbm_peak):
     op = sw.WilsonDirac(q, 0.1)
     out = op.normal(psi)
     ctx = _lib.ctx()
+    for _ in range(10):     # warm-up (inputs + U + output = 402 MB > L2: every rep streams HBM)
+        ctx.call("sch_ddagd", _lib.ptr(op.U), _lib.ptr(psi), _lib.ptr(out), B, L, L, 0.1)
     torch.cuda.synchronize()
-    reps = 20
+    reps = 50
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(reps):   # the C-ABI call itself, output preallocated
