@@ -46,10 +46,10 @@ PEAKS_PATH = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
 
 # DRAM bytes per lattice site of one resident-CG launch, measured by ncu
-# (profiles/r01/ncu_full_k_cg_resident.txt: 33.627136 MB read + 38.912 KB
+# (profiles/r01/ncu_full_k_cg_resident.txt: 33.579264 MB read + 8.704 KB
 # written for 2048 chains x 256 sites): U and b in, x out — the solve itself
 # never leaves the SM.
-NCU_CG_DRAM_BYTES_PER_SITE = (33.627136e6 + 38.912e3) / (2048 * 256)
+NCU_CG_DRAM_BYTES_PER_SITE = (33.579264e6 + 8.704e3) / (2048 * 256)
 
 CFG3 = dict(L=16, T=16, beta=2.0, m0=0.1, tau=1.0, scheme="adapted-nested-fg", micro_per_call=2,
             cg_tol=1e-10)
