@@ -30,6 +30,7 @@
 #include "tile.cuh"
 #include "tma_tile.cuh"
 #include "resident.cuh"
+#include "resident_col.cuh"
 #include <cstdio>
 #include <cstdlib>
 #include "../../include/schwinger_sm100.h"
@@ -56,12 +57,29 @@ int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
+template <int LC, int TC, int SPT, int MINB>
+int launch_rescol(sch_ctx* ctx, const ResArgs& a, int B) {
+  constexpr int NT = LC * TC / SPT;
+  const size_t smem = sizeof(double2) * 2 * (2 * SPT + 2) * NT;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_cg_rescol<LC, TC, SPT, MINB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  k_cg_rescol<LC, TC, SPT, MINB><<<B, NT, smem, ctx->stream>>>(a);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
 // Threads x sites-per-thread x min-CTAs-per-SM of the resident engine for V
 // sites; 16x16 and 32x32 get shape-specialised instantiations.
-// SCH_RESIDENT="NTxSPTxMINBxSPEC" overrides for tuning runs (SPEC 1 = use
-// the compile-time-shape kernel for this L x T, 0 = generic).
+// SCH_RESIDENT="NTxSPTxMINBxSPEC" overrides for tuning runs (SPEC 2 = the
+// column-owned kernel (resident_col.cuh), 1 = the compile-time-shape strided
+// kernel, 0 = generic).
 int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
-  static int fnt = -1, fspt = 0, fminb = 0, fspec = 1;
+  static int fnt = -1, fspt = 0, fminb = 0, fspec = 2;
   if (fnt < 0) {
     fnt = 0;
     if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%dx%dx%d", &fnt, &fspt, &fminb, &fspec);
@@ -74,6 +92,16 @@ int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
   else if (V <= 256) { nt = 128; spt = 2; minb = 4; }
   else if (V <= 512) { nt = 256; spt = 2; minb = 1; }
   else { nt = 256; spt = 4; minb = 1; }
+  const bool col = fnt > 0 && (long long)fnt * fspt >= V ? fspec == 2 : true;
+  if (col && a.L == 16 && a.T == 16) {
+    if (nt == 128 && spt == 2 && minb == 4) return launch_rescol<16, 16, 2, 4>(ctx, a, B);
+    if (nt == 128 && spt == 2 && minb == 5) return launch_rescol<16, 16, 2, 5>(ctx, a, B);
+    if (nt == 64 && spt == 4 && minb == 6) return launch_rescol<16, 16, 4, 6>(ctx, a, B);
+  }
+  if (col && a.L == 32 && a.T == 32) {
+    if (nt == 256 && spt == 4 && minb == 1) return launch_rescol<32, 32, 4, 1>(ctx, a, B);
+    if (nt == 512 && spt == 2 && minb == 1) return launch_rescol<32, 32, 2, 1>(ctx, a, B);
+  }
   const bool s16 = spec && a.L == 16 && a.T == 16 && (long long)nt * spt == 256;
   const bool s32 = spec && a.L == 32 && a.T == 32 && (long long)nt * spt == 1024;
 #define SCH_RES(N, S, M) \
