@@ -158,6 +158,35 @@ def cpu_baseline(seconds, outer):
                       f"{cores} processes x {seconds:.0f}s, oracle/schwinger_oracle.py"}
 
 
+def _cpu_stencil_worker(args):
+    """Oracle D^dag D on a slice of cfg2 (B_slice x 32^2) for ~seconds."""
+    seed, nb, seconds = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import schwinger_oracle as O
+    rng = np.random.default_rng(seed)
+    q = rng.uniform(-np.pi, np.pi, size=(nb, 2, 32, 32))
+    U = np.exp(1j * q)
+    psi = rng.standard_normal((nb, 32, 32, 2)) + 1j * rng.standard_normal((nb, 32, 32, 2))
+    n, t0 = 0, time.perf_counter()
+    while True:
+        O.normal_op(U, psi, 0.1)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return n * nb * 32 * 32, el
+
+
+def cpu_stencil_baseline(seconds):
+    cores = cpu_cores()
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        res = pool.map(_cpu_stencil_worker, [(c, 16, seconds) for c in range(cores)])
+    gbs = sum(96.0 * sites / el for sites, el in res) / 1e9
+    return {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"oracle normal_op (NumPy, batched) on 16 x 32x32 lattices per process, "
+                      f"{cores} processes x {seconds:.0f}s, 96 B/site"}
+
+
 def run_reference(args):
     """--impl reference: the CPU port of the reference path on all host cores."""
     rank = int(os.environ.get("RANK", "0"))
@@ -329,9 +358,11 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     hbm_peak, peak_kind = peaks()
 
-    cpu = None
+    cpu = cpu_stencil = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.cpu_seconds, args.outer)   # before CUDA init (fork-safe)
+        if not args.no_stencil:
+            cpu_stencil = cpu_stencil_baseline(min(args.cpu_seconds, 5.0))
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -347,6 +378,8 @@ def run_ours(args):
     stencil = None
     if rank == 0 and not args.no_stencil:   # fresh allocator / caches
         stencil = stencil_bench(torch, sw, _lib, hbm_peak)
+        if cpu_stencil is not None:
+            stencil["ddagd"]["cpu_baseline"] = cpu_stencil
 
     from paper_1512_03812_b200.ensemble import gather_observables, shard_chains, summarize
     shard = shard_chains(args.chains * world, world, rank)   # weak scaling: chains per GPU fixed

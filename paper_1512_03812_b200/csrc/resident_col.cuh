@@ -175,7 +175,12 @@ __global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
     bool check = true;
     if (!repl) {
       rs_new = block_sum<NT>(rsn, red[1]);
-      check = rs_new <= t2lo || (rs_new <= t2hi && sqrt(rs_new) <= target);
+      check = rs_new <= t2lo;
+      if (!check && rs_new <= t2hi) {   // inside the band: the exact test (asm keeps
+        double sq;                      // the compiler from hoisting the sqrt)
+        asm volatile("sqrt.rn.f64 %0, %1;" : "=d"(sq) : "d"(rs_new));
+        check = sq <= target;
+      }
     }
     if (check) {   // true residual b - A x (shared with the residual replacement)
       normal_op(x, w);

@@ -89,3 +89,57 @@ def summarize(obs: dict) -> dict:
     if "plaquette" in obs:
         out["plaquette"] = float(np.mean(obs["plaquette"]))
     return out
+
+
+# ---------------------------------------------------------------------------
+# checkpoint / resume
+# ---------------------------------------------------------------------------
+
+def save_checkpoint(path, q, rng, shard: ChainShard | None = None, trajectory: int = 0,
+                    meta: dict | None = None) -> None:
+    """Write a shard's links and its chains' RNG positions to one .npz.
+
+    ``rng`` is a ``NumpyDeviceRng`` (device streams) or a list of host
+    Generators (parity mode); either way the file stores NumPy Philox states,
+    so a run can resume on the GPU or be handed to the reference's own
+    ``hmc_update`` per chain.  Links are the reference layout (B, 2, L, T)."""
+    from .lattice import NumpyDeviceRng, to_numpy
+    qn = to_numpy(q)
+    states = rng.get_states() if isinstance(rng, NumpyDeviceRng) else [g.bit_generator.state for g in rng]
+    if len(states) != qn.shape[0]:
+        raise ValueError(f"{len(states)} RNG streams for {qn.shape[0]} chains")
+    shard = shard or ChainShard(0, 1, 0, qn.shape[0], qn.shape[0])
+    np.savez(path, format=np.array("schwinger-b200-ensemble v1"), q=qn,
+             ctr=np.stack([s["state"]["counter"] for s in states]).astype(np.uint64),
+             key=np.stack([s["state"]["key"] for s in states]).astype(np.uint64),
+             buf=np.stack([s["buffer"] for s in states]).astype(np.uint64),
+             pos=np.array([s["buffer_pos"] for s in states], dtype=np.int32),
+             shard=np.array([shard.rank, shard.world, shard.start, shard.count, shard.total]),
+             trajectory=np.int64(trajectory), meta=np.array(repr(meta or {})))
+
+
+def load_checkpoint(path, device_rng: bool = True):
+    """Inverse of ``save_checkpoint``: (q on the GPU, rng, shard, trajectory).
+
+    ``device_rng`` selects a ``NumpyDeviceRng`` continuing every stream on the
+    GPU; otherwise host Generators are returned."""
+    import ast
+    from .lattice import NumpyDeviceRng, as_links
+    z = np.load(path)
+    if str(z["format"]) != "schwinger-b200-ensemble v1":
+        raise ValueError(f"{path}: not an ensemble checkpoint")
+    states = [{"bit_generator": "Philox", "state": {"counter": z["ctr"][c], "key": z["key"][c]},
+               "buffer": z["buf"][c], "buffer_pos": int(z["pos"][c]), "has_uint32": 0,
+               "uinteger": 0} for c in range(z["ctr"].shape[0])]
+    if device_rng:
+        rng = NumpyDeviceRng(0, len(states))
+        rng.set_states(states)
+    else:
+        rng = []
+        for s in states:
+            g = np.random.Generator(np.random.Philox(key=[0, 0]))
+            g.bit_generator.state = s
+            rng.append(g)
+    r, w, start, count, total = (int(v) for v in z["shard"])
+    meta = ast.literal_eval(str(z["meta"]))
+    return as_links(z["q"]), rng, ChainShard(r, w, start, count, total), int(z["trajectory"]), meta

@@ -198,6 +198,8 @@ class NumpyDeviceRng:
         self.n = int(n_chains)
         self.seed, self.stream0 = int(seed) % 2**64, int(stream0) % 2**64
         nbytes = int(lib.sch_np_rng_state_bytes())
+        if nbytes != _NP_STATE_DTYPE.itemsize:
+            raise _lib.NativeUnavailable(f"device RNG state is {nbytes} B, host expects 88")
         self.state = torch.empty((self.n * nbytes,), dtype=torch.uint8, device=device())
         _lib.ctx().call("sch_np_rng_init", _lib.ptr(self.state), self.n, self.seed, self.stream0)
 
@@ -236,6 +238,77 @@ class NumpyDeviceRng:
         acc = torch.empty((self.n,), dtype=torch.int32, device=dh.device)
         _lib.ctx().call("sch_np_metropolis", _lib.ptr(self.state), _lib.ptr(dh), _lib.ptr(acc), self.n)
         return acc
+
+    # -- checkpointing: the per-chain Philox counters ----
+    # The device record is NumPy's own Philox state (counter[4], key[2],
+    # buffer[4], buffer_pos), so a chain's stream can be handed to or taken
+    # from a host np.random.Generator at any point and continue identically.
+
+    def get_states(self) -> list[dict]:
+        """Per-chain ``Generator.bit_generator.state`` dicts (Philox)."""
+        rec = _np_state_records(self.state.cpu().numpy())
+        out = []
+        for c in range(self.n):
+            out.append({"bit_generator": "Philox",
+                        "state": {"counter": rec["ctr"][c].copy(), "key": rec["key"][c].copy()},
+                        "buffer": rec["buf"][c].copy(), "buffer_pos": int(rec["pos"][c]),
+                        "has_uint32": 0, "uinteger": 0})
+        return out
+
+    def set_states(self, states) -> None:
+        """Load per-chain Philox state dicts (e.g. from reference Generators)."""
+        if len(states) != self.n:
+            raise ValueError(f"expected {self.n} states, got {len(states)}")
+        raw = np.zeros(self.state.numel(), dtype=np.uint8)
+        rec = _np_state_records(raw)
+        for c, s in enumerate(states):
+            if s.get("bit_generator") != "Philox":
+                raise ValueError("only Philox generator states can be loaded")
+            if s.get("has_uint32", 0):
+                raise ValueError("a pending 32-bit half word cannot be carried over")
+            rec["ctr"][c] = np.asarray(s["state"]["counter"], dtype=np.uint64)
+            rec["key"][c] = np.asarray(s["state"]["key"], dtype=np.uint64)
+            rec["buf"][c] = np.asarray(s["buffer"], dtype=np.uint64)
+            pos = int(s["buffer_pos"])
+            if not 0 <= pos <= 4:
+                raise ValueError(f"buffer_pos {pos} out of range")
+            rec["pos"][c] = pos
+        self.state.copy_(torch.from_numpy(raw).to(self.state.device))
+
+    @classmethod
+    def from_generators(cls, gens) -> "NumpyDeviceRng":
+        """Device streams continuing the given host Generators exactly."""
+        gens = list(gens)
+        self = cls(0, len(gens))
+        self.set_states([g.bit_generator.state for g in gens])
+        return self
+
+    def save(self, path) -> None:
+        """Write the per-chain counters/keys/buffers to an .npz checkpoint."""
+        rec = _np_state_records(self.state.cpu().numpy())
+        np.savez(path, ctr=rec["ctr"], key=rec["key"], buf=rec["buf"], pos=rec["pos"].astype(np.int32),
+                 seed=np.uint64(self.seed), stream0=np.uint64(self.stream0))
+
+    @classmethod
+    def load(cls, path) -> "NumpyDeviceRng":
+        z = np.load(path)
+        n = int(z["ctr"].shape[0])
+        self = cls(int(z["seed"]), n, int(z["stream0"]))
+        self.set_states([{"bit_generator": "Philox",
+                          "state": {"counter": z["ctr"][c], "key": z["key"][c]},
+                          "buffer": z["buf"][c], "buffer_pos": int(z["pos"][c])}
+                         for c in range(n)])
+        return self
+
+
+_NP_STATE_DTYPE = np.dtype([("ctr", "<u8", (4,)), ("key", "<u8", (2,)), ("buf", "<u8", (4,)),
+                            ("pos", "<i4"), ("pad", "<i4")])   # csrc/nprng.cu NpPhilox (88 B)
+
+
+def _np_state_records(raw: np.ndarray) -> np.ndarray:
+    """View a device-state byte image as NpPhilox records (no copy)."""
+    assert _NP_STATE_DTYPE.itemsize == 88
+    return raw.view(_NP_STATE_DTYPE)
 
 
 # ---------------------------------------------------------------------------

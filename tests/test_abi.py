@@ -3,6 +3,8 @@ symbol include/schwinger_sm100.h declares, and the ctypes table matches the
 header one to one."""
 
 import ctypes
+
+import numpy as np
 import re
 from pathlib import Path
 
@@ -77,3 +79,14 @@ def test_package_does_not_import_oracle():
         src = f.read_text()
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\S+)", src, re.M), f
         assert "schwinger_oracle" not in src, f
+
+
+def test_np_rng_state_layout_matches_host_view():
+    """The device Philox record is NumPy's state in 88 B (host view in lattice.py)."""
+    from paper_1512_03812_b200 import _lib, lattice
+    assert int(_lib.load().sch_np_rng_state_bytes()) == lattice._NP_STATE_DTYPE.itemsize == 88
+    raw = np.zeros(2 * 88, dtype=np.uint8)
+    rec = lattice._np_state_records(raw)
+    rec["ctr"][1] = [1, 2, 3, 4]
+    rec["pos"][1] = 3
+    assert raw[88:96].view("<u8")[0] == 1 and raw[88 + 80:88 + 84].view("<i4")[0] == 3

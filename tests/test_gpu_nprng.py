@@ -86,3 +86,80 @@ def test_device_stream_ensemble_matches_reference_chains():
         assert np.max(np.abs(st.dh - np.array([s["dh"] for s in so]))) < 1e-8
         assert np.array_equal(st.accepted, np.array([s["accepted"] for s in so]))
     assert np.max(np.abs(q.cpu().numpy() - qo)) < 1e-8
+
+
+def test_rng_state_export_continues_on_host():
+    """get_states() are NumPy Philox states: a host Generator built from one
+    continues the device stream draw for draw (checkpoint / hand-back)."""
+    import paper_1512_03812_b200 as sw
+    g = sw.NumpyDeviceRng(seed=99, n_chains=4, stream0=10)
+    g.standard_normal((1001,))   # odd count: leaves a partly used buffer
+    g.random()
+    states = g.get_states()
+    dev = g.standard_normal((513,)).cpu().numpy()
+    for c in range(4):
+        ref = sw.make_rng(99, 10 + c)
+        ref.standard_normal(1001)
+        ref.random()
+        assert states[c]["buffer_pos"] == ref.bit_generator.state["buffer_pos"]
+        assert np.array_equal(states[c]["state"]["counter"], ref.bit_generator.state["state"]["counter"])
+        h = np.random.Generator(np.random.Philox(key=[0, 0]))
+        h.bit_generator.state = states[c]
+        assert np.array_equal(h.standard_normal(513), dev[c])
+
+
+def test_rng_from_host_generators_and_npz_checkpoint(tmp_path):
+    import paper_1512_03812_b200 as sw
+    gens = [sw.make_rng(5, s) for s in (3, 8, 21)]
+    for i, h in enumerate(gens):   # advance each host stream differently
+        h.standard_normal(17 * (i + 1))
+        h.uniform(-1.0, 1.0, size=i)
+    d = sw.NumpyDeviceRng.from_generators(gens)
+    a = d.standard_normal((64,)).cpu().numpy()
+    d.save(tmp_path / "rng.npz")
+    b = d.uniform(-np.pi, np.pi, (40,)).cpu().numpy()
+    d2 = sw.NumpyDeviceRng.load(tmp_path / "rng.npz")
+    b2 = d2.uniform(-np.pi, np.pi, (40,)).cpu().numpy()
+    assert np.array_equal(b, b2)
+    for c, h in enumerate(gens):
+        assert np.array_equal(a[c], h.standard_normal(64))
+        assert np.array_equal(b[c], h.uniform(-np.pi, np.pi, size=40))
+    with pytest.raises(ValueError):
+        d.set_states(d.get_states()[:2])
+
+
+def test_ensemble_checkpoint_resume_and_hand_back_to_reference(tmp_path):
+    """save_checkpoint after 2 device trajectories; resuming it on the GPU is
+    bit-identical to the uninterrupted run, and the same file loaded with host
+    generators continues chain by chain in the CPU oracle (dH <= 1e-8, same
+    accept sequence)."""
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200 import ensemble as E
+    from oracle import schwinger_oracle as O
+    B, L = 3, 8
+    cfg = sw.HmcConfig(L=L, T=L, beta=2.0, m0=0.1, tau=1.0, h=1.0 / 3.0, scheme="adapted-nested-fg",
+                       micro_per_call=2, cg_tol=1e-10)
+    ocfg = O.Config(L=L, T=L, beta=2.0, m0=0.1, tau=1.0, h=1.0 / 3.0, scheme="adapted-nested-fg",
+                    micro_per_call=2, cg_tol=1e-10)
+    g = sw.NumpyDeviceRng(seed=4242, n_chains=B)
+    q = g.hot_start(sw.LatticeGeom(L, L))
+    for _ in range(2):
+        q, _ = sw.hmc_update_ensemble(q, cfg, device_rng=g)
+    E.save_checkpoint(tmp_path / "ck.npz", q, g, trajectory=2, meta={"beta": 2.0})
+    qa = q
+    dha = []
+    for _ in range(2):
+        qa, st = sw.hmc_update_ensemble(qa, cfg, device_rng=g)
+        dha.append(st.dh)
+    qb, gb, shard, traj, meta = E.load_checkpoint(tmp_path / "ck.npz")
+    assert traj == 2 and meta == {"beta": 2.0} and shard.count == B
+    for k in range(2):
+        qb, st = sw.hmc_update_ensemble(qb, cfg, device_rng=gb)
+        assert np.array_equal(st.dh, dha[k])
+    assert torch.equal(qa, qb)
+    qo, rngs, _, _, _ = E.load_checkpoint(tmp_path / "ck.npz", device_rng=False)
+    qo = qo.cpu().numpy()
+    for k in range(2):
+        qo, so = O.ensemble_update(qo, ocfg, rngs)
+        assert np.max(np.abs(dha[k] - np.array([s["dh"] for s in so]))) < 1e-8
+    assert np.max(np.abs(qa.cpu().numpy() - qo)) < 1e-8
