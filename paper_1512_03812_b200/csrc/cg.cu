@@ -57,50 +57,54 @@ int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
-template <int LC, int TC, int SPT, int MINB>
-int launch_rescol(sch_ctx* ctx, const ResArgs& a, int B) {
-  constexpr int NT = LC * TC / SPT;
-  const size_t smem = sizeof(double2) * 2 * (2 * SPT + 2) * NT;
+template <int LC, int TC, int BX, int BT, int MINB>
+int launch_resblk(sch_ctx* ctx, const ResArgs& a, int B) {
+  constexpr int NT = LC * TC / (BX * BT);
+  const size_t smem = sizeof(double2) * 2 * (2 * BT + 2 * BX) * NT;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cg_rescol<LC, TC, SPT, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  k_cg_rescol<LC, TC, SPT, MINB><<<B, NT, smem, ctx->stream>>>(a);
+  k_cg_resblk<LC, TC, BX, BT, MINB><<<B, NT, smem, ctx->stream>>>(a);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
 
 // Threads x sites-per-thread x min-CTAs-per-SM of the resident engine for V
-// sites; 16x16 and 32x32 get shape-specialised instantiations.
-// SCH_RESIDENT="NTxSPTxMINBxSPEC" overrides for tuning runs (SPEC 2 = the
-// column-owned kernel (resident_col.cuh), 1 = the compile-time-shape strided
-// kernel, 0 = generic).
+// sites; 16x16 and 32x32 get shape-specialised block-owned instantiations.
+// SCH_RESIDENT="NTxSPTxMINBxSPEC" overrides for tuning runs: SPEC 2 = block-
+// owned kernel with 1 x SPT blocks (resident_col.cuh), 3 = 2 x SPT/2 blocks,
+// 1 = the compile-time-shape strided kernel, 0 = generic.
 int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
-  static int fnt = -1, fspt = 0, fminb = 0, fspec = 2;
+  static int fnt = -1, fspt = 0, fminb = 0, fspec = 3;
   if (fnt < 0) {
     fnt = 0;
     if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%dx%dx%d", &fnt, &fspt, &fminb, &fspec);
   }
+  const bool forced = fnt > 0 && (long long)fnt * fspt >= V;
   int nt, spt, minb;
   bool spec = true;
-  if (fnt > 0 && (long long)fnt * fspt >= V) {
+  if (forced) {
     nt = fnt; spt = fspt; minb = fminb; spec = fspec != 0;
   } else if (V <= 128) { nt = 128; spt = 1; minb = 1; }
+  else if (V == 256 && a.L == 16) { nt = 64; spt = 4; minb = 4; }
   else if (V <= 256) { nt = 128; spt = 2; minb = 4; }
   else if (V <= 512) { nt = 256; spt = 2; minb = 1; }
   else { nt = 256; spt = 4; minb = 1; }
-  const bool col = fnt > 0 && (long long)fnt * fspt >= V ? fspec == 2 : true;
-  if (col && a.L == 16 && a.T == 16) {
-    if (nt == 128 && spt == 2 && minb == 4) return launch_rescol<16, 16, 2, 4>(ctx, a, B);
-    if (nt == 128 && spt == 2 && minb == 5) return launch_rescol<16, 16, 2, 5>(ctx, a, B);
-    if (nt == 64 && spt == 4 && minb == 6) return launch_rescol<16, 16, 4, 6>(ctx, a, B);
+  const int blk = forced ? fspec : 3;   // 2: 1 x SPT, 3: 2 x SPT/2
+  if (a.L == 16 && a.T == 16) {
+    if (blk == 2 && nt == 128 && spt == 2 && minb == 4) return launch_resblk<16, 16, 1, 2, 4>(ctx, a, B);
+    if (blk == 2 && nt == 64 && spt == 4 && minb == 4) return launch_resblk<16, 16, 1, 4, 4>(ctx, a, B);
+    if (blk == 3 && nt == 64 && spt == 4 && minb == 4) return launch_resblk<16, 16, 2, 2, 4>(ctx, a, B);
+    if (blk == 3 && nt == 128 && spt == 2 && minb == 4) return launch_resblk<16, 16, 2, 1, 4>(ctx, a, B);
   }
-  if (col && a.L == 32 && a.T == 32) {
-    if (nt == 256 && spt == 4 && minb == 1) return launch_rescol<32, 32, 4, 1>(ctx, a, B);
-    if (nt == 512 && spt == 2 && minb == 1) return launch_rescol<32, 32, 2, 1>(ctx, a, B);
+  if (a.L == 32 && a.T == 32) {
+    if (blk == 2 && nt == 256 && spt == 4 && minb == 1) return launch_resblk<32, 32, 1, 4, 1>(ctx, a, B);
+    if (blk == 3 && nt == 256 && spt == 4 && minb == 1) return launch_resblk<32, 32, 2, 2, 1>(ctx, a, B);
+    if (blk == 2 && nt == 512 && spt == 2 && minb == 1) return launch_resblk<32, 32, 1, 2, 1>(ctx, a, B);
   }
   const bool s16 = spec && a.L == 16 && a.T == 16 && (long long)nt * spt == 256;
   const bool s32 = spec && a.L == 32 && a.T == 32 && (long long)nt * spt == 1024;

@@ -143,9 +143,9 @@ SCH_DEV double block_sum(double v, double* slot) {
   v = warp_sum(v);
   if ((threadIdx.x & 31) == 0) slot[threadIdx.x >> 5] = v;
   __syncthreads();
-  double s = 0.0;
+  double s = slot[0];
 #pragma unroll
-  for (int w = 0; w < NW; ++w) s += slot[w];
+  for (int w = 1; w < NW; ++w) s += slot[w];
   return s;
 }
 

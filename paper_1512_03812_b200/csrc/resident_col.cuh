@@ -1,17 +1,20 @@
-// Resident per-chain CG, column-owned variant (the 16^2 / 32^2 hot shapes).
+// Resident per-chain CG, block-owned variant (the 16^2 / 32^2 hot shapes).
 //
 // Same algorithm, stopping rule and data placement as k_cg_resident
-// (resident.cuh), but each thread owns SPT t-consecutive sites of one x row
-// ("column segment") instead of SPT sites strided by the block size.  The
-// t-hops between a thread's own sites then never leave its registers: per
-// D application a segment exports
-//   plane 0 / plane 1 (read by x-1 / x+1)  for all SPT sites
-//   plane 2           (read by t-1)        for its first site only
-//   plane 3           (read by t+1)        for its last site only
-// i.e. 2*SPT+2 projected components instead of 4*SPT (SPT=2: -25 % shared
-// memory traffic, SPT=4: -37.5 %).  Shared-memory planes are indexed by
-// thread id, so every warp-wide store and neighbour load touches one
-// contiguous (or 8-lane-permuted) 512-B run: conflict-free.
+// (resident.cuh), but each thread owns a BX x BT block of sites (BX rows in
+// x, BT consecutive sites in t) instead of sites strided by the block size.
+// Hops between a thread's own sites never leave its registers; per D
+// application a block exports to shared memory only its faces:
+//   plane 0 (read by x-1): the BT sites of its first row
+//   plane 1 (read by x+1): the BT sites of its last row
+//   plane 2 (read by t-1): the BX sites of its first column
+//   plane 3 (read by t+1): the BX sites of its last column
+// i.e. 2(BX+BT) projected components per BX*BT sites instead of 4 per site
+// (1x2: -25 %, 1x4: -37.5 %, 2x2: -50 % shared-memory traffic).  Internal
+// hops are formed after the barrier straight from the neighbour site's
+// registers, so nothing extra stays live across it.  Planes are indexed by
+// thread id: every warp-wide store and neighbour load is one contiguous (or
+// lane-permuted within aligned 128-B groups) run — conflict-free.
 //
 // The per-iteration stopping test sqrt(rs') <= target (fermion.py:202) is
 // decided without the square root unless rs' falls inside a +-4e-15 band
@@ -19,16 +22,21 @@
 // the one the reference takes, at two compares per iteration.
 #pragma once
 
+#include <type_traits>
+
 #include "resident.cuh"
 
-template <int LC, int TC, int SPT, int MINB>
-__global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
+template <int LC, int TC, int BX, int BT, int MINB>
+__global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs a) {
+  constexpr int SPT = BX * BT;
   constexpr int NT = LC * TC / SPT;
-  constexpr int NSEG = TC / SPT;
+  constexpr int NBT = TC / BT, NBX = LC / BX;
   constexpr int V = LC * TC;
   constexpr int NW = NT / 32;
-  constexpr int PL = (2 * SPT + 2) * NT;   // double2 per exchange stage
-  static_assert(TC % SPT == 0 && NT % 32 == 0, "segment shape");
+  constexpr int PL = (2 * BT + 2 * BX) * NT;   // double2 per exchange stage
+  static_assert(TC % BT == 0 && LC % BX == 0 && NT % 32 == 0, "block shape");
+  // plane offsets inside one stage
+  constexpr int O0 = 0, O1 = BT * NT, O2 = 2 * BT * NT, O3 = (2 * BT + BX) * NT;
   extern __shared__ double2 sm[];
   __shared__ double red[3][NW];
   double2* E0 = sm;
@@ -36,23 +44,22 @@ __global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
   const int tid = threadIdx.x;
   const int c = blockIdx.x;
   const long long cb = (long long)c * V;
-  const int xx = tid / NSEG, seg = tid % NSEG;
-  const int s0 = xx * TC + seg * SPT;
-  // exchange partners (thread ids owning the neighbouring segments)
-  const int txp = ((xx + 1) % LC) * NSEG + seg;
-  const int txm = ((xx + LC - 1) % LC) * NSEG + seg;
-  const int ttp = xx * NSEG + (seg + 1) % NSEG;
-  const int ttm = xx * NSEG + (seg + NSEG - 1) % NSEG;
-  constexpr int OX1 = SPT * NT, OT0 = 2 * SPT * NT, OT1 = (2 * SPT + 1) * NT;
+  const int bx = tid / NBT, bt = tid % NBT;
+  auto site = [&](int k) { return (bx * BX + k / BT) * TC + bt * BT + k % BT; };
+  // exchange partners (thread ids owning the neighbouring blocks)
+  const int txp = ((bx + 1) % NBX) * NBT + bt;
+  const int txm = ((bx + NBX - 1) % NBX) * NBT + bt;
+  const int ttp = bx * NBT + (bt + 1) % NBT;
+  const int ttm = bx * NBT + (bt + NBT - 1) % NBT;
 
   double2 u0[SPT], u1[SPT];
   Spinor x[SPT], r[SPT], p[SPT];
   double bb = 0.0;
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
-    u0[k] = cscale(-0.5, __ldg(a.U + 2 * cb + s0 + k));   // exact: power-of-two scale
-    u1[k] = cscale(-0.5, __ldg(a.U + 2 * cb + V + s0 + k));
-    r[k] = ldg_spinor(a.b, cb + s0 + k);
+    u0[k] = cscale(-0.5, __ldg(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
+    u1[k] = cscale(-0.5, __ldg(a.U + 2 * cb + V + site(k)));
+    r[k] = ldg_spinor(a.b, cb + site(k));
     x[k].s0 = x[k].s1 = make_double2(0, 0);
     bb += spinor_norm2(r[k]);
   }
@@ -61,7 +68,7 @@ __global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
   const double target = a.tol * normb;
   if (normb == 0.0) {   // fermion.py:181-182, per chain
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + s0 + k, x[k]);
+    for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), x[k]);
     if (tid == 0) {
       a.iters[c] = 0;
       a.relres[c] = 0.0;
@@ -72,30 +79,49 @@ __global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
   const double t2 = target * target;
   const double t2lo = t2 * (1.0 - 4e-15), t2hi = t2 * (1.0 + 4e-15);
 
-  // ---- one D (DAG=false) or D^dag (DAG=true) exchange stage
-  // produce: write this segment's exports of v into E, keep the t-internal
-  // ones in registers
-  auto produce = [&](auto dag, double2* E, const Spinor* v, double2* f2, double2* f3) {
-    constexpr bool DAG = decltype(dag)::value;
+  // The four exports of site k (D: DAG=false, D^dag: DAG=true), res_produce
+  // order: e0 = w_f0(v), e1 = conj(u0) w_b0(v), e2 = w_f1(v), e3 = conj(u1) w_b1(v)
+  auto e0 = [&](auto dag, const Spinor& v) {
+    return decltype(dag)::value ? wplus0(v) : wminus0(v);
+  };
+  auto e1 = [&](auto dag, const Spinor& v, int k) {
+    return cmulc(u0[k], decltype(dag)::value ? wminus0(v) : wplus0(v));
+  };
+  auto e2 = [&](auto dag, const Spinor& v) {
+    return decltype(dag)::value ? wplus1(v) : wminus1(v);
+  };
+  auto e3 = [&](auto dag, const Spinor& v, int k) {
+    return cmulc(u1[k], decltype(dag)::value ? wminus1(v) : wplus1(v));
+  };
+  // produce: the block's face exports of v
+  auto produce = [&](auto dag, double2* E, const Spinor* v) {
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-      E[k * NT + tid] = DAG ? wplus0(v[k]) : wminus0(v[k]);
-      E[OX1 + k * NT + tid] = cmulc(u0[k], DAG ? wminus0(v[k]) : wplus0(v[k]));
-      const double2 a2 = DAG ? wplus1(v[k]) : wminus1(v[k]);
-      const double2 a3 = cmulc(u1[k], DAG ? wminus1(v[k]) : wplus1(v[k]));
-      if (k == 0) E[OT0 + tid] = a2;
-      else f2[k] = a2;
-      if (k == SPT - 1) E[OT1 + tid] = a3;
-      else f3[k] = a3;
+      const int i = k / BT, j = k % BT;
+      if (i == 0) E[O0 + j * NT + tid] = e0(dag, v[k]);
+      if (i == BX - 1) E[O1 + j * NT + tid] = e1(dag, v[k], k);
+      if (j == 0) E[O2 + i * NT + tid] = e2(dag, v[k]);
+      if (j == BT - 1) E[O3 + i * NT + tid] = e3(dag, v[k], k);
     }
   };
-  auto gather = [&](const double2* E, const double2* f2, const double2* f3, Hops* h) {
+  // gather: the four hops of every site (faces from shared memory, internal
+  // ones from the neighbour site's registers)
+  auto gather = [&](auto dag, const double2* E, const Spinor* v, Hops* h) {
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-      h[k].f0 = E[k * NT + txp];
-      h[k].b0 = E[OX1 + k * NT + txm];
-      h[k].f1 = (k == SPT - 1) ? E[OT0 + ttp] : f2[k + 1];
-      h[k].b1 = (k == 0) ? E[OT1 + ttm] : f3[k - 1];
+      const int i = k / BT, j = k % BT;
+      if (i == BX - 1) h[k].f0 = E[O0 + j * NT + txp];
+      if (i == 0) h[k].b0 = E[O1 + j * NT + txm];
+      if (j == BT - 1) h[k].f1 = E[O2 + i * NT + ttp];
+      if (j == 0) h[k].b1 = E[O3 + i * NT + ttm];
+    }
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      const int i = k / BT, j = k % BT;
+      if (i < BX - 1) h[k].f0 = e0(dag, v[k + BT]);
+      if (i > 0) h[k].b0 = e1(dag, v[k - BT], k - BT);
+      if (j < BT - 1) h[k].f1 = e2(dag, v[k + 1]);
+      if (j > 0) h[k].b1 = e3(dag, v[k - 1], k - 1);
     }
   };
   using F = std::integral_constant<bool, false>;
@@ -104,16 +130,15 @@ __global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
   // out = D^dag D v (two exchange rounds).  Precondition: every thread has
   // finished reading E0/E1 of the previous application.
   auto normal_op = [&](const Spinor* v, Spinor* out) {
-    double2 f2[SPT], f3[SPT];
     Hops h[SPT];
-    produce(F{}, E0, v, f2, f3);
+    produce(F{}, E0, v);
     __syncthreads();
-    gather(E0, f2, f3, h);
+    gather(F{}, E0, v, h);
 #pragma unroll
     for (int k = 0; k < SPT; ++k) out[k] = res_combine<false>(h[k], v[k], u0[k], u1[k], a.diag);
-    produce(T{}, E1, out, f2, f3);
+    produce(T{}, E1, out);
     __syncthreads();
-    gather(E1, f2, f3, h);
+    gather(T{}, E1, out, h);
 #pragma unroll
     for (int k = 0; k < SPT; ++k) out[k] = res_combine<true>(h[k], out[k], u0[k], u1[k], a.diag);
   };
@@ -122,7 +147,7 @@ __global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
   double rs = normb2;   // r = b exactly: the same sum as ||b||^2 (fermion.py:186,191)
   if (a.x0) {
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) x[k] = ldg_spinor(a.x0, cb + s0 + k);
+    for (int k = 0; k < SPT; ++k) x[k] = ldg_spinor(a.x0, cb + site(k));
     normal_op(x, w);
     double rr = 0.0;
 #pragma unroll
@@ -136,30 +161,30 @@ __global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
   for (int k = 0; k < SPT; ++k) p[k] = r[k];
 
   double best = INFINITY;
+  double inv_rs = __drcp_rn(rs);
   for (int it = 1; it <= a.maxiter; ++it) {
     // w = D^dag D p; <p, D^dag D p> formed as ||D p||^2 during the D stage
     // and published by the barrier between the stages (resident.cuh)
-    double2 f2[SPT], f3[SPT];
     Hops h[SPT];
-    produce(F{}, E0, p, f2, f3);
+    produce(F{}, E0, p);
     __syncthreads();
-    gather(E0, f2, f3, h);
+    gather(F{}, E0, p, h);
     double dd = 0.0;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       w[k] = res_combine<false>(h[k], p[k], u0[k], u1[k], a.diag);
       dd += spinor_norm2(w[k]);
     }
-    produce(T{}, E1, w, f2, f3);
+    produce(T{}, E1, w);
     dd = warp_sum(dd);
     if ((tid & 31) == 0) red[0][tid >> 5] = dd;
     __syncthreads();
-    gather(E1, f2, f3, h);
+    gather(T{}, E1, w, h);
 #pragma unroll
     for (int k = 0; k < SPT; ++k) w[k] = res_combine<true>(h[k], w[k], u0[k], u1[k], a.diag);
-    double den = 0.0;
+    double den = red[0][0];
 #pragma unroll
-    for (int q = 0; q < NW; ++q) den += red[0][q];
+    for (int q = 1; q < NW; ++q) den += red[0][q];
     const double alpha = den > 0.0 ? rs / den : 0.0;
     const bool repl = (it % kResReplace) == 0;
     double rsn = 0.0;
@@ -187,7 +212,7 @@ __global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
       double tn2 = 0.0;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
-        w[k] = sp_sub(ldg_spinor(a.b, cb + s0 + k), w[k]);
+        w[k] = sp_sub(ldg_spinor(a.b, cb + site(k)), w[k]);
         tn2 += spinor_norm2(w[k]);
       }
       tn2 = block_sum<NT>(tn2, red[2]);
@@ -195,7 +220,7 @@ __global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
       if (!repl || tn <= target) best = tn / normb;
       if (tn <= target) {
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + s0 + k, x[k]);
+        for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), x[k]);
         if (tid == 0) {
           a.iters[c] = it;
           a.relres[c] = tn / normb;
@@ -207,13 +232,21 @@ __global__ void __launch_bounds__(LC * TC / SPT, MINB) k_cg_rescol(ResArgs a) {
       for (int k = 0; k < SPT; ++k) r[k] = w[k];
       rs_new = tn2;
     }
-    const double beta = rs > 0.0 ? rs_new / rs : 0.0;
+    // rs'/rs finished from the reciprocal formed off the critical path:
+    // q0 = rs'*y, rem = rs' - rs*q0 (exact), q = q0 + rem*y -- the correctly
+    // rounded quotient for y = RN(1/rs) (Markstein), in 3 dependent ops
+    double beta = 0.0;
+    if (rs > 0.0) {
+      const double q0 = rs_new * inv_rs;
+      beta = __fma_rn(__fma_rn(-rs, q0, rs_new), inv_rs, q0);
+    }
 #pragma unroll
     for (int k = 0; k < SPT; ++k) p[k] = sp_fma(beta, p[k], r[k]);
     rs = rs_new;
+    inv_rs = __drcp_rn(rs);
   }
 #pragma unroll
-  for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + s0 + k, x[k]);
+  for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), x[k]);
   if (tid == 0) {
     a.iters[c] = a.maxiter;
     a.relres[c] = fmin(best, sqrt(rs) / normb);
