@@ -80,6 +80,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stencil", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--streams", type=int, default=1,
+                    help="sub-ensembles issued concurrently on separate streams (measured "
+                         "slower than 1 on cfg3: 2 -> -6 %%, profiles/r01/README.md)")
     ap.add_argument("--strips", type=int, default=1, help="cfg5: strips on one GPU (local transport)")
     ap.add_argument("--cfg5-size", type=int, default=2048)
     args = ap.parse_args()
@@ -388,11 +391,37 @@ def run_ours(args):
     geom = sw.LatticeGeom(cfg.L, cfg.T)
     # chain c draws exactly the reference's make_rng(2024, c) stream, on device:
     # hot start first, then every trajectory's heatbaths and Metropolis draw
-    drng = sw.NumpyDeviceRng(seed=2024, n_chains=chains, stream0=shard.start)
-    q = drng.hot_start(geom)
+    # The shard can be issued as S contiguous sub-ensembles on S streams (each
+    # with its own library context) so their kernels interleave on the GPU.
+    # Chain c keeps stream c: results do not depend on S.  Default S=1: the
+    # small kernels then squeeze resident-CG CTAs off the SMs and the step
+    # gets slower (S=2: 164.5k -> 154.3k chain-traj/s).
+    S = max(1, min(args.streams, chains))
+    subs = [shard_chains(chains, S, i) for i in range(S)]
+    main = torch.cuda.current_stream()
+    streams = [torch.cuda.Stream() for _ in range(S)] if S > 1 else [main]
+    drngs, qs = [], []
+    for sub, stm in zip(subs, streams):
+        stm.wait_stream(main)
+        with torch.cuda.stream(stm):
+            d = sw.NumpyDeviceRng(seed=2024, n_chains=sub.count, stream0=shard.start + sub.start)
+            drngs.append(d)
+            qs.append(d.hot_start(geom))
+
+    def ensemble_step(qs, uploads=None):
+        pend = []
+        for i, stm in enumerate(streams):
+            stm.wait_stream(main)
+            with torch.cuda.stream(stm):
+                qi = qs[i] if uploads is None else uploads[i]()
+                qs[i], p = sw.hmc_update_ensemble_async(qi, cfg, drngs[i])
+                pend.append(p)
+        for stm in streams:
+            main.wait_stream(stm)
+        return [p.resolve() for p in pend]
 
     for _ in range(args.warmup):
-        q, st = sw.hmc_update_ensemble(q, cfg, device_rng=drng)
+        sts = ensemble_step(qs)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -405,9 +434,10 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        q, st = sw.hmc_update_ensemble(q, cfg, device_rng=drng)
-        acc.append(st.accepted)
-        dhs.append(st.dh)
+        sts = ensemble_step(qs)
+        acc.append(np.concatenate([st.accepted for st in sts]))
+        dhs.append(np.concatenate([st.dh for st in sts]))
+    st = sts[0]
     e1.record()
     torch.cuda.synchronize()
     barrier()
@@ -422,8 +452,20 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = chains * world / (ms_step * 1e-3)
 
-    # dominant kernel: the resident CG (one launch per solve)
-    cg_ms = sum(a.elapsed_time(b) for a, b, _, _ in prof)
+    # dominant kernel: the resident CG (one launch per solve).  Its time is
+    # the union of the CG launch intervals (they overlap across streams), so
+    # achieved = CG bytes / time during which a CG kernel was running.
+    spans = sorted((e0.elapsed_time(a), e0.elapsed_time(b)) for a, b, _, _ in prof)
+    cg_ms, cur = 0.0, None
+    for a0, b0 in spans:
+        if cur is None or a0 > cur[1]:
+            if cur is not None:
+                cg_ms += cur[1] - cur[0]
+            cur = [a0, b0]
+        else:
+            cur[1] = max(cur[1], b0)
+    if cur is not None:
+        cg_ms += cur[1] - cur[0]
     cg_iters = sum(int(it.sum().item()) for _, _, it, _ in prof)
     V = cfg.L * cfg.T
     n_solves = len(prof)
@@ -443,18 +485,21 @@ def run_ours(args):
     # e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
-        q_host = q.cpu().pin_memory()
-        q_back = torch.empty_like(q_host).pin_memory()
-        h2d = q_host.numel() * 8
+        q_host = [qi.cpu().pin_memory() for qi in qs]
+        q_back = [torch.empty_like(h).pin_memory() for h in q_host]
+        h2d = sum(h.numel() for h in q_host) * 8
         steps_e2e = max(2, args.steps // 2)
+        uploads = [lambda h=h: h.to("cuda", non_blocking=True) for h in q_host]
         barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
         for _ in range(steps_e2e):
-            qd = q_host.to("cuda", non_blocking=True)
-            qd, st = sw.hmc_update_ensemble(qd, cfg, device_rng=drng)
-            q_back.copy_(qd, non_blocking=True)
+            ensemble_step(qs, uploads)   # host links in, per-chain dH / accept out
+            for i, stm in enumerate(streams):
+                with torch.cuda.stream(stm):
+                    q_back[i].copy_(qs[i], non_blocking=True)
+                main.wait_stream(stm)
         f1.record()
         torch.cuda.synchronize()
         barrier()
@@ -463,7 +508,7 @@ def run_ours(args):
             t = torch.tensor([ems], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        d2h = q_back.numel() * 8 + chains * (8 + 4)
+        d2h = sum(b.numel() for b in q_back) * 8 + chains * (8 + 4)
         e2e = {"value": chains * world / (ems / steps_e2e * 1e-3), "unit": "chain-trajectories/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems / steps_e2e}

@@ -87,9 +87,9 @@ class NativeUnavailable(RuntimeError):
     """The sm_100a library or the CUDA device is missing: there is no fallback."""
 
 
-_lock = threading.Lock()
+_lock = threading.RLock()
 _lib = None
-_contexts: dict[int, "Context"] = {}
+_contexts: dict[tuple[int, int], "Context"] = {}
 
 
 def load() -> ctypes.CDLL:
@@ -115,9 +115,12 @@ def exported_symbols() -> list[str]:
 
 
 class Context:
-    """One sch_ctx per CUDA device; calls follow torch's current stream."""
+    """One sch_ctx per (CUDA device, stream): a context's workspace arena,
+    graph cache and poll flag are only ever touched in its own stream's
+    order, so work issued on different torch streams runs concurrently
+    without sharing scratch memory."""
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, stream: int):
         lib = load()
         if not torch.cuda.is_available():
             raise NativeUnavailable("no CUDA device: the B200 path has no CPU fallback")
@@ -130,16 +133,10 @@ class Context:
         self.lib = lib
         self.handle = handle
         self.device = device
-        self._stream = None
-
-    def _bind_stream(self):
-        s = torch.cuda.current_stream(self.device).cuda_stream
-        if s != self._stream:
-            self.lib.sch_set_stream(self.handle, _c_ptr(s))
-            self._stream = s
+        self.stream = stream
+        lib.sch_set_stream(handle, _c_ptr(stream))
 
     def call(self, name: str, *args):
-        self._bind_stream()
         rc = getattr(self.lib, name)(self.handle, *args)
         if rc != 0:
             msg = self.lib.sch_last_error(self.handle).decode(errors="replace")
@@ -154,12 +151,17 @@ class Context:
 
 
 def ctx(device: int | None = None) -> Context:
+    """The context of torch's current stream on ``device``."""
     if device is None:
         device = torch.cuda.current_device()
-    c = _contexts.get(device)
+    key = (device, torch.cuda.current_stream(device).cuda_stream)
+    c = _contexts.get(key)
     if c is None:
-        c = Context(device)
-        _contexts[device] = c
+        with _lock:
+            c = _contexts.get(key)
+            if c is None:
+                c = Context(device, key[1])
+                _contexts[key] = c
     return c
 
 

@@ -191,14 +191,59 @@ def hmc_update_ensemble(q, config: HmcConfig, rngs=None, device_rng: DeviceRng |
     exactly the draws an unbatched ``hmc_update`` would make.  Bench mode:
     ``device_rng`` draws momenta, pseudofermions and Metropolis uniforms on
     the GPU.  Returns (links, EnsembleStats)."""
+    if (rngs is None) == (device_rng is None):
+        raise ValueError("pass exactly one of rngs (parity mode) or device_rng (bench mode)")
+    if device_rng is not None:
+        out, pending = hmc_update_ensemble_async(q, config, device_rng, counter, reuse_solves)
+        return out, pending.resolve()
+    return _ensemble_update(q, config, rngs, None, counter, reuse_solves, sync=True)
+
+
+class PendingEnsembleStats:
+    """Outcome of an ensemble update issued without any host synchronisation:
+    per-chain dH and accept flags still on the device.  ``resolve()`` reads
+    them back, raises SolverError / ValueError exactly as the synchronous
+    call would, and returns the EnsembleStats."""
+
+    def __init__(self, state, result, dh_dev, acc_dev, t0):
+        self._state, self._result = state, result
+        self.dh_dev, self.acc_dev = dh_dev, acc_dev
+        self._t0 = t0
+        self._stream = torch.cuda.current_stream(dh_dev.device)
+        self._stats = None
+
+    def resolve(self) -> "EnsembleStats":
+        if self._stats is None:
+            with torch.cuda.stream(self._stream):   # read back in the issuing stream's order
+                self._state.check_solves()
+                dh = self.dh_dev.cpu().numpy()
+                acc_h = self.acc_dev.cpu().numpy()
+            if (acc_h < 0).any():
+                raise ValueError(f"non-finite energy change {dh[acc_h < 0][0]}")
+            self._stats = EnsembleStats(dh=dh, accepted=acc_h == 1,
+                                        inversions=self._result.inversions,
+                                        n_steps=self._result.n_steps,
+                                        wall_time=time.perf_counter() - self._t0)
+        return self._stats
+
+
+def hmc_update_ensemble_async(q, config: HmcConfig, device_rng, counter=None,
+                              reuse_solves: bool = True):
+    """Bench-mode ensemble update, issued on torch's current stream with no
+    host round trip: returns (links, PendingEnsembleStats).  Sub-ensembles
+    issued on different streams run concurrently (each stream has its own
+    library context), which fills the GPU during one another's CG tails and
+    small kernels.  Rejected / non-finite chains keep their input links."""
+    return _ensemble_update(q, config, None, device_rng, counter, reuse_solves, sync=False)
+
+
+def _ensemble_update(q, config, rngs, device_rng, counter, reuse_solves, sync):
     q = as_links(q)
     if q.ndim != 4:
         raise ValueError("hmc_update_ensemble expects links of shape (B, 2, L, T)")
     B = q.shape[0]
     geom = LatticeGeom(config.L, config.T)
     counter = counter if counter is not None else InversionCounter()
-    if (rngs is None) == (device_rng is None):
-        raise ValueError("pass exactly one of rngs (parity mode) or device_rng (bench mode)")
     if rngs is not None:
         if len(rngs) != B:
             raise ValueError(f"need one generator per chain ({B}), got {len(rngs)}")
@@ -236,17 +281,15 @@ def hmc_update_ensemble(q, config: HmcConfig, rngs=None, device_rng: DeviceRng |
             u = device_rng.uniform(B)
             acc = torch.empty((B,), dtype=torch.int32, device=q.device)
             _lib.ctx().call("sch_metropolis", _lib.ptr(dh_dev), _lib.ptr(u), _lib.ptr(acc), B)
-        state.check_solves()
-        dh = dh_dev.cpu().numpy()
-        acc_h = acc.cpu().numpy()
-        if (acc_h < 0).any():
-            raise ValueError(f"non-finite energy change {dh[acc_h < 0][0]}")
-        accepted = acc_h == 1
-    else:
-        state.check_solves()
-        dh = dh_dev.cpu().numpy()
-        accepted = np.array([metropolis(float(d), r) for d, r in zip(dh, rngs)], dtype=bool)
-        acc = torch.from_numpy(accepted.astype(np.int32)).to(q.device)
+        out = torch.empty_like(q)
+        _lib.ctx().call("sch_select_chains", _lib.ptr(acc), _lib.ptr(state.q), _lib.ptr(q),
+                        _lib.ptr(out), B, q[0].numel())
+        pending = PendingEnsembleStats(state, result, dh_dev, acc, t0)
+        return (out, pending.resolve()) if sync else (out, pending)
+    state.check_solves()
+    dh = dh_dev.cpu().numpy()
+    accepted = np.array([metropolis(float(d), r) for d, r in zip(dh, rngs)], dtype=bool)
+    acc = torch.from_numpy(accepted.astype(np.int32)).to(q.device)
     out = torch.empty_like(q)
     _lib.ctx().call("sch_select_chains", _lib.ptr(acc), _lib.ptr(state.q), _lib.ptr(q),
                     _lib.ptr(out), B, q[0].numel())
