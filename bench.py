@@ -45,11 +45,24 @@ sys.path.insert(0, str(ROOT))
 PEAKS_PATH = ROOT / "MEASURED_PEAKS.json"
 FALLBACK_HBM = 6650.0
 
-# DRAM bytes per lattice site of one resident-CG launch, measured by ncu
-# (profiles/r01/ncu_full_k_cg_resident.txt: 33.579264 MB read + 8.704 KB
-# written for 2048 chains x 256 sites): U and b in, x out — the solve itself
-# never leaves the SM.
-NCU_CG_DRAM_BYTES_PER_SITE = (33.579264e6 + 8.704e3) / (2048 * 256)
+# The dominant kernel of each ensemble workload, and the DRAM bytes per
+# lattice site of one of its launches measured by ncu --set full (U and b
+# in, x out — the solve itself stays on chip):
+#   cfg3: profiles/r01/ncu_full_k_cg_resblk.txt, 33.590016 MB read + 6.144 KB
+#         written for 2048 chains x 256 sites
+#   cfg4: profiles/r01/ncu_full_k_cg_cluster.txt, 268.64384 MB read +
+#         104.760064 MB written for 1024 chains x 4096 sites (b is re-read by
+#         the true-residual checks; part of it misses L2)
+CG_KERNELS = {
+    "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread> (per-chain CG, one 64-thread CTA "
+                        "per chain, 4 CTAs/SM)",
+                 dram_per_site=(33.590016e6 + 6.144e3) / (2048 * 256),
+                 source="profiles/r01/ncu_full_k_cg_resblk.txt"),
+    "cfg4": dict(kernel="k_cg_cluster<64,64,4 CTAs,2x2 sites/thread> (per-chain CG, one 4-CTA "
+                        "cluster per chain, DSMEM faces)",
+                 dram_per_site=(268.64384e6 + 104.760064e6) / (1024 * 4096),
+                 source="profiles/r01/ncu_full_k_cg_cluster.txt"),
+}
 
 CFG3 = dict(L=16, T=16, beta=2.0, m0=0.1, tau=1.0, scheme="adapted-nested-fg", micro_per_call=2,
             cg_tol=1e-10)
@@ -535,14 +548,14 @@ def run_ours(args):
                        "cg_iterations_per_chain_traj": cg_iters / (chains * args.steps)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak,
-                         "traffic": NCU_CG_DRAM_BYTES_PER_SITE * V * chains,
+                         "traffic": CG_KERNELS[args.workload]["dram_per_site"] * V * chains,
                          "traffic_source": "dram__bytes_read.sum+dram__bytes_write.sum of one "
-                                           "k_cg_resident launch (ncu --set full, 2048 chains, "
-                                           "profiles/r01/ncu_full_k_cg_resident.txt), per site, "
+                                           "launch (ncu --set full, "
+                                           f"{CG_KERNELS[args.workload]['source']}), per site, "
                                            "x sites of one launch here",
                          "algorithmic_bytes_per_launch": cg_bytes / max(1, n_solves),
                          "peak_kind": peak_kind,
-                         "kernel": "k_cg_resident (per-chain CG, one CTA per chain)",
+                         "kernel": CG_KERNELS[args.workload]["kernel"],
                          "bytes_model": "352 B/site/CG-iteration (SURVEY 8(d)), "
                                         f"{V} sites x {cg_iters} chain-iterations",
                          "effective": True,

@@ -31,6 +31,7 @@
 #include "tma_tile.cuh"
 #include "resident.cuh"
 #include "resident_col.cuh"
+#include "resident_cluster.cuh"
 #include <cstdio>
 #include <cstdlib>
 #include "../../include/schwinger_sm100.h"
@@ -122,6 +123,40 @@ int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
 #undef SCH_RES16
 #undef SCH_RES32
   return sch_fail(ctx, SCH_ERR_ARG, "no resident CG instantiation %dx%dx%d", nt, spt, minb);
+}
+
+// Cluster-resident CG (resident_cluster.cuh): CS CTAs per chain.
+template <int LC, int TC, int CS, int BX, int BT, int MINB>
+int launch_cluster(sch_ctx* ctx, const ResArgs& a, int B) {
+  constexpr int NT = LC * TC / (CS * BX * BT);
+  const size_t smem = sizeof(double2) * 2 * (2 * BT + 2 * BX) * NT;
+  auto kern = k_cg_cluster<LC, TC, CS, BX, BT, MINB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess && CS > 8)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "cluster attr: %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  kern<<<B * CS, NT, smem, ctx->stream>>>(a);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+// 64^2 (cfg4): which cluster shape; SCH_CLUSTER=0 falls back to streaming
+int cluster_dispatch(sch_ctx* ctx, const ResArgs& a, int B) {
+  static int cs = -1;
+  if (cs < 0) {
+    cs = 4;   // measured: 4 CTAs (1 per SM) 78.5 ns/chain-iteration, 8: 85, 16: 141 (spills)
+    if (const char* e = getenv("SCH_CLUSTER")) cs = atoi(e);
+  }
+  if (a.L == 64 && a.T == 64) {
+    if (cs == 8) return launch_cluster<64, 64, 8, 2, 2, 2>(ctx, a, B);
+    if (cs == 16) return launch_cluster<64, 64, 16, 2, 2, 4>(ctx, a, B);
+    if (cs == 4) return launch_cluster<64, 64, 4, 2, 2, 1>(ctx, a, B);
+  }
+  return -1;   // no cluster instantiation: use the streaming engine
 }
 
 // =========================================================== streaming CG
@@ -677,7 +712,13 @@ extern "C" int sch_cg_normal(sch_ctx* ctx, const double* U, const double* b, dou
     ResArgs a{(const double2*)U, (const double2*)b, (const double2*)x0, (double2*)x, iters, relres,
               status, L, T, 2.0 + m0, tol, maxiter};
     rc = resident_dispatch(ctx, a, B, V);
+  } else if (per_chain && (rc = cluster_dispatch(ctx, ResArgs{(const double2*)U, (const double2*)b,
+                                                              (const double2*)x0, (double2*)x, iters,
+                                                              relres, status, L, T, 2.0 + m0, tol,
+                                                              maxiter}, B)) >= 0) {
+    // cluster-resident engine ran (rc = its status)
   } else {
+    rc = SCH_OK;
     rc = cg_streaming(ctx, (const double2*)U, (const double2*)b, (double2*)x, (const double2*)x0, B,
                       L, T, m0, tol, maxiter, per_chain ? 0 : 1, iters, relres, status);
   }

@@ -103,6 +103,26 @@ SCH_DEV Spinor res_combine(const Hops& h, const Spinor& v, double2 u0, double2 u
   return r;
 }
 
+// Incremental form of res_combine: o accumulates one site's hops one at a
+// time, diag*v fused into the first, so the hops a thread already holds (its
+// internal ones) can be summed while an exchange barrier is pending.
+// KIND 0: forward x (h = U0(n) * export), 1: backward x, 2: forward t,
+// 3: backward t.  Spin-1 coefficients: D f0 -1, b0 +1, f1 -i, b1 +i; D^dag
+// the negatives (fermion.py:101-117).
+template <bool DAG, int KIND>
+SCH_DEV void hop_acc(Spinor& o, double2 h, bool first, const Spinor& v, double diag) {
+  constexpr bool neg = (KIND == 0 || KIND == 2) != DAG;
+  double2 g = KIND >= 2 ? cmuli(h) : h;
+  if (neg) g = make_double2(-g.x, -g.y);
+  if (first) {
+    o.s0 = make_double2(__fma_rn(diag, v.s0.x, h.x), __fma_rn(diag, v.s0.y, h.y));
+    o.s1 = make_double2(__fma_rn(diag, v.s1.x, g.x), __fma_rn(diag, v.s1.y, g.y));
+  } else {
+    o.s0 = cadd(o.s0, h);
+    o.s1 = cadd(o.s1, g);
+  }
+}
+
 SCH_DEV Spinor sp_fma(double a, const Spinor& p, const Spinor& x) {   // a*p + x
   Spinor r;
   r.s0 = make_double2(__fma_rn(a, p.s0.x, x.s0.x), __fma_rn(a, p.s0.y, x.s0.y));

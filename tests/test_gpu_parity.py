@@ -171,6 +171,30 @@ def test_cg_streaming_engine_matches_oracle(sw):
     assert rel_err(npy(x), xo) < TOL_OP
 
 
+@pytest.mark.parametrize("m0", [0.1, 0.02])
+def test_cg_cluster_engine_matches_oracle(sw, m0):
+    """64^2 per-chain solves run on the cluster-resident engine (8 CTAs per
+    chain, DSMEM faces): iteration counts identical to the oracle's per-chain
+    CG, x within 1e-12; a zero right-hand side and a warm start included."""
+    from oracle import schwinger_oracle as O
+    rng = np.random.default_rng(64)
+    q = rng.uniform(-np.pi, np.pi, (3, 2, 64, 64))
+    b = rng.standard_normal((3, 64, 64, 2)) + 1j * rng.standard_normal((3, 64, 64, 2))
+    b[1] = 0.0
+    op = sw.WilsonDirac(q, m0)
+    x, its, _ = sw.cg_normal(op, b, 1e-10, stop="per_chain")
+    xo, itso, _ = O.cg_normal(O.fermion_links(q), m0, b, 1e-10, stop="per_chain")
+    assert np.array_equal(its, itso) and its[1] == 0 and its.max() > 50
+    assert rel_err(npy(x), xo) < TOL_OP
+    x0 = xo + 1e-3 * rng.standard_normal(xo.shape)
+    xw, itw, _ = sw.cg_normal(op, b, 1e-10, x0=x0, stop="per_chain")
+    xwo, itwo, _ = O.cg_normal(O.fermion_links(q), m0, b, 1e-10, x0=x0, stop="per_chain")
+    assert np.array_equal(itw, itwo)
+    assert rel_err(npy(xw), xwo) < TOL_OP
+    with pytest.raises(sw.SolverError):
+        sw.cg_normal(op, b, 1e-10, maxiter=5, stop="per_chain")
+
+
 @pytest.mark.parametrize("tag", ["u", "b"])
 def test_forces_match_reference(sw, golden, tag):
     g = golden("forces")
