@@ -50,17 +50,19 @@ FALLBACK_HBM = 6650.0
 # in, x out — the solve itself stays on chip):
 #   cfg3: profiles/r01/ncu_full_k_cg_resblk.txt, 33.590016 MB read + 6.144 KB
 #         written for 2048 chains x 256 sites
-#   cfg4: profiles/r01/ncu_full_k_cg_cluster.txt, 268.64384 MB read +
-#         104.760064 MB written for 1024 chains x 4096 sites (b is re-read by
+#   cfg4: profiles/r01/ncu_full_k_cg_cluster.txt, 268.8832 MB read +
+#         103.359744 MB written for 1024 chains x 4096 sites (b is re-read by
 #         the true-residual checks; part of it misses L2)
+DRAM_CFG4 = (268.8832e6 + 103.359744e6) / (1024 * 4096)
 CG_KERNELS = {
     "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread> (per-chain CG, one 64-thread CTA "
                         "per chain, 4 CTAs/SM)",
                  dram_per_site=(33.590016e6 + 6.144e3) / (2048 * 256),
                  source="profiles/r01/ncu_full_k_cg_resblk.txt"),
-    "cfg4": dict(kernel="k_cg_cluster<64,64,4 CTAs,2x2 sites/thread> (per-chain CG, one 4-CTA "
-                        "cluster per chain, DSMEM faces)",
-                 dram_per_site=(268.64384e6 + 104.760064e6) / (1024 * 4096),
+    "cfg4": dict(kernel="k_cg_cluster_tx<64,64,4 CTAs,2x2 sites/thread> (per-chain CG, one "
+                        "4-CTA cluster per chain, faces and partial sums pushed with st.async "
+                        "onto the receiver's mbarrier)",
+                 dram_per_site=DRAM_CFG4,
                  source="profiles/r01/ncu_full_k_cg_cluster.txt"),
 }
 
@@ -161,6 +163,12 @@ def cpu_cores():
         return os.cpu_count() or 1
 
 
+def _phys_label(outer):
+    c = CFG3
+    return (f"{c['L']}x{c['T']} chains, beta={c['beta']}, m0={c['m0']}, tau={c['tau']}, "
+            f"{c['scheme']} {outer}x{c['micro_per_call']} steps, tol {c['cg_tol']:g}")
+
+
 def cpu_baseline(seconds, outer):
     cores = cpu_cores()
     ctx = mp.get_context("fork")
@@ -169,9 +177,9 @@ def cpu_baseline(seconds, outer):
     n = sum(r[0] for r in res)
     rate = sum(r[0] / r[1] for r in res)
     return {"value": rate, "unit": "chain-trajectories/s", "cores": cores, "kind": "port",
-            "sample": f"{n} unbatched hmc_update trajectories of independent 16x16 hot-start "
-                      f"chains (cfg3 physics, adapted-nested-fg, {outer}x2 steps, tol 1e-10), "
-                      f"{cores} processes x {seconds:.0f}s, oracle/schwinger_oracle.py"}
+            "sample": f"{n} unbatched hmc_update trajectories of independent hot-start "
+                      f"{_phys_label(outer)}, {cores} processes x {seconds:.0f}s, "
+                      "oracle/schwinger_oracle.py"}
 
 
 def _cpu_stencil_worker(args):
@@ -225,8 +233,8 @@ def run_reference(args):
         "unit": "chain-trajectories/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64/c128", "data": "synthetic",
-        "config": {"workload": "cfg3: independent 16x16 chains, beta=2.0, m0=0.1, tau=1, "
-                               f"adapted-nested-fg {args.outer}x2 steps, tol 1e-10, hot start",
+        "config": {"workload": f"{args.workload}: independent {_phys_label(args.outer)}, "
+                               "hot start",
                    "chains_per_step": cores},
         "cpu_baseline": {"value": value, "unit": "chain-trajectories/s", "cores": cores,
                          "kind": "port",

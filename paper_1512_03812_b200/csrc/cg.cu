@@ -144,12 +144,43 @@ int launch_cluster(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
-// 64^2 (cfg4): which cluster shape; SCH_CLUSTER=0 falls back to streaming
+template <int LC, int TC, int CS, int BX, int BT, int MINB>
+int launch_cluster_tx(sch_ctx* ctx, const ResArgs& a, int B) {
+  constexpr int NT = LC * TC / (CS * BX * BT);
+  constexpr int PL = (2 * BT + 2 * BX) * NT;
+  constexpr int FACE = BT * (TC / BT);
+  const size_t smem = sizeof(double2) * (2 * PL + 8 * FACE);
+  auto kern = k_cg_cluster_tx<LC, TC, CS, BX, BT, MINB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess && CS > 8)
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "cluster attr: %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  kern<<<B * CS, NT, smem, ctx->stream>>>(a);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+// 64^2 (cfg4): which cluster shape; SCH_CLUSTER=0 falls back to streaming,
+// SCH_CLUSTER_SYNC=1 selects the cluster-barrier variant
 int cluster_dispatch(sch_ctx* ctx, const ResArgs& a, int B) {
   static int cs = -1;
   if (cs < 0) {
-    cs = 4;   // measured: 4 CTAs (1 per SM) 78.5 ns/chain-iteration, 8: 85, 16: 141 (spills)
+    cs = 4;   // measured (cfg4 shape): st.async/mbarrier variant 4 CTAs 67.2 ns/chain-iteration,
+              // 8 CTAs 67.8; cluster-barrier variant 4: 78.5, 8: 85, 16: 141 (spills)
     if (const char* e = getenv("SCH_CLUSTER")) cs = atoi(e);
+  }
+  static int sync_mode = -1;
+  if (sync_mode < 0) {
+    const char* e = getenv("SCH_CLUSTER_SYNC");
+    sync_mode = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (a.L == 64 && a.T == 64 && !sync_mode) {
+    if (cs == 4) return launch_cluster_tx<64, 64, 4, 2, 2, 1>(ctx, a, B);
+    if (cs == 8) return launch_cluster_tx<64, 64, 8, 2, 2, 2>(ctx, a, B);
   }
   if (a.L == 64 && a.T == 64) {
     if (cs == 8) return launch_cluster<64, 64, 8, 2, 2, 2>(ctx, a, B);
