@@ -521,6 +521,13 @@ __global__ void k_iter_inc(StreamState st) {
   if (threadIdx.x == 0) ++*st.it;
 }
 
+// Body tail of the device-side CG loop: keep iterating while a chain is
+// active (the WHILE node of the conditional graph re-evaluates this).
+__global__ void k_set_continue(StreamState st, cudaGraphConditionalHandle h) {
+  if (threadIdx.x == 0)
+    cudaGraphSetConditional(h, (*st.n_active > 0 && *st.it <= st.maxiter + 1) ? 1u : 0u);
+}
+
 // Chains whose rhs is exactly zero return x = 0 (fermion.py:181-182): per
 // chain in per-chain mode, and for the whole batch in global mode when every
 // rhs is zero.
@@ -682,7 +689,45 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
     return *ctx->h_flag == 0 ? 1 : 0;
   };
 
-  if (use_cg_graph()) {
+  if (use_cg_graph() && use_cg_while()) {
+    // The whole loop on the device: a conditional WHILE node whose body is
+    // kBody captured iterations plus k_set_continue.  One graph launch per
+    // solve, no host polling: the call returns without synchronising.
+    const int kBody = tpc * B >= 4096 ? 1 : 4;   // big batches: exact trip count
+    if (!ctx->cap_stream)
+      SCH_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    SCH_CUDA(ctx, cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle handle;
+    SCH_CUDA(ctx, cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    SCH_CUDA(ctx, cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SCH_CUDA(ctx, cudaStreamBeginCaptureToGraph(ctx->cap_stream, body, nullptr, nullptr, 0,
+                                                cudaStreamCaptureModeRelaxed));
+    int per = 0;
+    for (int j = 0; j < kBody; ++j) per += enqueue_iteration(ctx->cap_stream);
+    k_set_continue<<<1, 32, 0, ctx->cap_stream>>>(st, handle);
+    cudaError_t ce = cudaGetLastError();
+    SCH_CUDA(ctx, cudaStreamEndCapture(ctx->cap_stream, &body));
+    if (ce != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      return sch_fail(ctx, SCH_ERR_CUDA, "cg while-capture: %s", cudaGetErrorString(ce));
+    }
+    cudaGraphExec_t exec;
+    cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "cg while-instantiate: %s", cudaGetErrorString(ie));
+    cudaError_t le = cudaGraphLaunch(exec, s);
+    cudaGraphExecDestroy(exec);   // released once the launch completes
+    if (le != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "cg graph launch: %s", cudaGetErrorString(le));
+    ctx->launches += per + 1;     // per body pass; the trip count is decided on the device
+  } else if (use_cg_graph()) {
     // capture kChunk iterations once on a private stream, replay on s
     constexpr int kChunk = 8;
     if (!ctx->cap_stream)

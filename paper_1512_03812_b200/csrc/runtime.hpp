@@ -118,6 +118,17 @@ inline bool use_cg_graph() {
   return v == 1;
 }
 
+// The streaming CG runs its loop on the device through a conditional WHILE
+// graph node; SCH_CG_WHILE=0 replays fixed chunks with host polling instead.
+inline bool use_cg_while() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCH_CG_WHILE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // The streaming CG's stencil pass measured faster with the per-tile kernel
 // (profiles/r01/README.md); SCH_TMA_CG=1 switches it to the TMA pipeline.
 inline bool use_tma_cg() {
