@@ -373,6 +373,41 @@ def stencil_bench(torch, sw, _lib, hbm_peak):
     return res
 
 
+def graph_bench(torch, sw, reps=10):
+    """Small ensembles are launch-bound: one HMC update (cfg3 physics) per
+    step eagerly vs replayed as one captured CUDA graph (EnsembleUpdateGraph)."""
+    cfg = sw.HmcConfig(h=0.25, **{k: v for k, v in CFG3.items()})
+    geom = sw.LatticeGeom(cfg.L, cfg.T)
+    out = {"workload": f"cfg3 physics ({cfg.L}x{cfg.T}, adapted-nested-fg 4x2), one update per step"}
+    if cfg.L * cfg.T > 1024:
+        return None
+    for B in (1, 64):
+        d = sw.NumpyDeviceRng(seed=5, n_chains=B)
+        q = d.hot_start(geom)
+        for _ in range(2):
+            q, _ = sw.hmc_update_ensemble(q, cfg, device_rng=d)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            q, p = sw.hmc_update_ensemble_async(q, cfg, d)
+        e1.record()
+        torch.cuda.synchronize()
+        eager = e0.elapsed_time(e1) / reps
+        upd = sw.EnsembleUpdateGraph(q, cfg, d)
+        upd.step()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            upd.step()
+        e1.record()
+        torch.cuda.synchronize()
+        graph = e0.elapsed_time(e1) / reps
+        out[f"B{B}"] = {"eager_ms_per_update": eager, "graph_ms_per_update": graph,
+                        "speedup": eager / graph}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -534,6 +569,10 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems / steps_e2e}
 
+    graphs = None
+    if rank == 0 and not args.no_stencil:
+        graphs = graph_bench(torch, sw)
+
     if rank == 0:
         line = {
             "metric": "HMC trajectories/s", "value": value, "unit": "chain-trajectories/s",
@@ -578,6 +617,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clk,
             "stencil": stencil,
+            "graph_capture": graphs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

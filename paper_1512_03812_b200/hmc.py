@@ -271,7 +271,7 @@ def _ensemble_update(q, config, rngs, device_rng, counter, reuse_solves, sync):
                     reuse_solves=reuse_solves)
     t0 = time.perf_counter()
     h_start = hamiltonian(state)
-    result = integrate_trajectory(state, _spec_of(config), config.tau)
+    result = integrate_trajectory(state, _spec_of(config), config.tau, check=sync)
     h_end = hamiltonian(state)
     dh_dev = h_end - h_start
     if device_rng is not None:
@@ -296,3 +296,64 @@ def _ensemble_update(q, config, rngs, device_rng, counter, reuse_solves, sync):
     wall = time.perf_counter() - t0
     return out, EnsembleStats(dh=dh, accepted=accepted, inversions=result.inversions,
                               n_steps=result.n_steps, wall_time=wall)
+
+
+class EnsembleUpdateGraph:
+    """One ensemble HMC update captured once as a CUDA graph and replayed
+    (whole-trajectory on-device execution).
+
+    ``step()`` replays heatbaths, both Hamiltonians, the whole trajectory,
+    Metropolis and the accept/reject select with one graph launch: no Python,
+    no per-kernel launch cost, the chains' state (links, the NumPy-stream
+    RNG) advancing in place on the device.  Values are identical to
+    ``hmc_update_ensemble`` with the same ``NumpyDeviceRng``.  Requires the
+    resident or cluster-resident CG engines (V <= 1024, or 64^2): the
+    streaming engine runs its own device-side graph."""
+
+    def __init__(self, q, config: HmcConfig, device_rng: NumpyDeviceRng, reuse_solves: bool = True):
+        if not isinstance(device_rng, NumpyDeviceRng):
+            raise TypeError("graph capture needs the device-resident NumpyDeviceRng streams")
+        V = config.L * config.T
+        if not (V <= 1024 or (config.L == 64 and config.T == 64)):
+            raise ValueError("graph capture needs a resident CG engine (V <= 1024 or 64x64)")
+        self.q = as_links(q).clone()
+        self.rng = device_rng
+        self.config = config
+        self._stream = torch.cuda.Stream()
+        main = torch.cuda.current_stream()
+        self._stream.wait_stream(main)
+        saved = device_rng.state.clone()
+        with torch.cuda.stream(self._stream):   # warm-up: library context, workspace, attributes
+            hmc_update_ensemble_async(self.q, config, device_rng, InversionCounter(), reuse_solves)
+        self._stream.synchronize()
+        device_rng.state.copy_(saved)            # the warm-up's draws are given back
+        self.graph = torch.cuda.CUDAGraph()
+        counter = InversionCounter()
+        with torch.cuda.graph(self.graph, stream=self._stream):
+            out, pend = hmc_update_ensemble_async(self.q, config, device_rng, counter, reuse_solves)
+            self.q.copy_(out)
+        self._pending = pend
+        self._infos = list(pend._state._infos)
+        self.inversions = pend._result.inversions
+        self.n_steps = pend._result.n_steps
+        main.wait_stream(self._stream)
+
+    def step(self):
+        """Replay one update on the current stream; returns the pending
+        per-chain (dH, accept) tensors (read them with ``stats()``)."""
+        self.graph.replay()
+        return self._pending.dh_dev, self._pending.acc_dev
+
+    def stats(self) -> "EnsembleStats":
+        """Host read-back of the last replay (raises like hmc_update_ensemble)."""
+        if self._infos:
+            bad = torch.stack([i.status_dev.ne(0).any() for i in self._infos]).any()
+            if bool(bad.item()):
+                for i in self._infos:
+                    i.raise_if_failed()
+        dh = self._pending.dh_dev.cpu().numpy()
+        acc = self._pending.acc_dev.cpu().numpy()
+        if (acc < 0).any():
+            raise ValueError(f"non-finite energy change {dh[acc < 0][0]}")
+        return EnsembleStats(dh=dh, accepted=acc == 1, inversions=self.inversions,
+                             n_steps=self.n_steps, wall_time=float("nan"))

@@ -370,9 +370,12 @@ step_nested_fg = SCHEMES["nested-fg"]
 step_adapted_nested_fg = SCHEMES["adapted-nested-fg"]
 
 
-def integrate_trajectory(state: MdState, spec: IntegratorSpec, tau: float) -> TrajectoryResult:
+def integrate_trajectory(state: MdState, spec: IntegratorSpec, tau: float,
+                         check: bool = True) -> TrajectoryResult:
     """round(tau/h) macro steps in place; returns the step count, the
-    inversions spent (reference convention) and n_steps*h (integrators.py:365-382)."""
+    inversions spent (reference convention) and n_steps*h (integrators.py:365-382).
+    ``check=False`` leaves the SolverError check of the trajectory's solves to
+    the caller (``state.check_solves()``), so nothing synchronises with the host."""
     if not tau > 0:
         raise ValueError(f"trajectory length must be positive, got {tau}")
     n_steps = max(1, round(tau / spec.h))
@@ -381,6 +384,7 @@ def integrate_trajectory(state: MdState, spec: IntegratorSpec, tau: float) -> Tr
     before = state.counter.count
     for _ in range(n_steps):
         step(state, spec.h, m, spec.fg_coefficient)
-    state.check_solves()
+    if check:
+        state.check_solves()
     return TrajectoryResult(n_steps=n_steps, inversions=state.counter.count - before,
                             realized_tau=n_steps * spec.h)

@@ -47,3 +47,29 @@ def test_two_streams_match_one_batch():
     assert torch.equal(torch.cat(qs), q1)
     keys = [k for k in _lib._contexts if k[0] == torch.cuda.current_device()]
     assert len(keys) >= 3   # default stream + the two side streams
+
+
+@pytest.mark.parametrize("L", [8, 16])
+def test_captured_update_graph_matches_eager(L):
+    """EnsembleUpdateGraph (one CUDA-graph replay per HMC update) gives the
+    values of eager hmc_update_ensemble on the same device streams."""
+    import paper_1512_03812_b200 as sw
+    B = 4
+    cfg = sw.HmcConfig(L=L, T=L, beta=2.0, m0=0.1, tau=1.0, h=0.25, scheme="adapted-nested-fg",
+                       micro_per_call=2, cg_tol=1e-10)
+    geom = sw.LatticeGeom(L, L)
+    ge = sw.NumpyDeviceRng(seed=77, n_chains=B)
+    qe = ge.hot_start(geom)
+    gg = sw.NumpyDeviceRng(seed=77, n_chains=B)
+    qg = gg.hot_start(geom)
+    upd = sw.EnsembleUpdateGraph(qg, cfg, gg)
+    assert torch.equal(gg.state, ge.state)      # capture consumed no draws
+    for _ in range(3):
+        qe, st = sw.hmc_update_ensemble(qe, cfg, device_rng=ge)
+        upd.step()
+        sg = upd.stats()
+        assert np.array_equal(sg.dh, st.dh)
+        assert np.array_equal(sg.accepted, st.accepted)
+        assert sg.inversions == st.inversions
+    assert torch.equal(upd.q, qe)
+    assert torch.equal(gg.state, ge.state)
