@@ -58,18 +58,18 @@ int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
-template <int LC, int TC, int BX, int BT, int MINB>
+template <int LC, int TC, int BX, int BT, int MINB, bool INC = false>
 int launch_resblk(sch_ctx* ctx, const ResArgs& a, int B) {
   constexpr int NT = LC * TC / (BX * BT);
   const size_t smem = sizeof(double2) * 2 * (2 * BT + 2 * BX) * NT;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB, INC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  k_cg_resblk<LC, TC, BX, BT, MINB><<<B, NT, smem, ctx->stream>>>(a);
+  k_cg_resblk<LC, TC, BX, BT, MINB, INC><<<B, NT, smem, ctx->stream>>>(a);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
@@ -78,9 +78,11 @@ int launch_resblk(sch_ctx* ctx, const ResArgs& a, int B) {
 // sites; 16x16 and 32x32 get shape-specialised block-owned instantiations.
 // SCH_RESIDENT="NTxSPTxMINBxSPEC" overrides for tuning runs: SPEC 2 = block-
 // owned kernel with 1 x SPT blocks (resident_col.cuh), 3 = 2 x SPT/2 blocks,
-// 1 = the compile-time-shape strided kernel, 0 = generic.
+// 4 = 2 x SPT/2 with the incremental combine (default; 16^2 2.26 ns,
+// 32^2 10.76 ns per chain-iteration), 1 = the compile-time-shape strided
+// kernel, 0 = generic.
 int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
-  static int fnt = -1, fspt = 0, fminb = 0, fspec = 3;
+  static int fnt = -1, fspt = 0, fminb = 0, fspec = 4;
   if (fnt < 0) {
     fnt = 0;
     if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%dx%dx%d", &fnt, &fspt, &fminb, &fspec);
@@ -95,16 +97,19 @@ int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
   else if (V <= 256) { nt = 128; spt = 2; minb = 4; }
   else if (V <= 512) { nt = 256; spt = 2; minb = 1; }
   else { nt = 256; spt = 4; minb = 1; }
-  const int blk = forced ? fspec : 3;   // 2: 1 x SPT, 3: 2 x SPT/2
+  const int blk = forced ? fspec : 4;   // 2: 1 x SPT, 3: 2 x SPT/2, 4: 2 x SPT/2 incremental
   if (a.L == 16 && a.T == 16) {
     if (blk == 2 && nt == 128 && spt == 2 && minb == 4) return launch_resblk<16, 16, 1, 2, 4>(ctx, a, B);
     if (blk == 2 && nt == 64 && spt == 4 && minb == 4) return launch_resblk<16, 16, 1, 4, 4>(ctx, a, B);
     if (blk == 3 && nt == 64 && spt == 4 && minb == 4) return launch_resblk<16, 16, 2, 2, 4>(ctx, a, B);
+    if (blk == 4 && nt == 64 && spt == 4 && minb == 4) return launch_resblk<16, 16, 2, 2, 4, true>(ctx, a, B);
+    if (blk == 4 && nt == 64 && spt == 4 && minb == 5) return launch_resblk<16, 16, 2, 2, 5, true>(ctx, a, B);
     if (blk == 3 && nt == 128 && spt == 2 && minb == 4) return launch_resblk<16, 16, 2, 1, 4>(ctx, a, B);
   }
   if (a.L == 32 && a.T == 32) {
     if (blk == 2 && nt == 256 && spt == 4 && minb == 1) return launch_resblk<32, 32, 1, 4, 1>(ctx, a, B);
     if (blk == 3 && nt == 256 && spt == 4 && minb == 1) return launch_resblk<32, 32, 2, 2, 1>(ctx, a, B);
+    if (blk == 4 && nt == 256 && spt == 4 && minb == 1) return launch_resblk<32, 32, 2, 2, 1, true>(ctx, a, B);
     if (blk == 2 && nt == 512 && spt == 2 && minb == 1) return launch_resblk<32, 32, 1, 2, 1>(ctx, a, B);
   }
   const bool s16 = spec && a.L == 16 && a.T == 16 && (long long)nt * spt == 256;

@@ -26,7 +26,7 @@
 
 #include "resident.cuh"
 
-template <int LC, int TC, int BX, int BT, int MINB>
+template <int LC, int TC, int BX, int BT, int MINB, bool INC = false>
 __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs a) {
   constexpr int SPT = BX * BT;
   constexpr int NT = LC * TC / SPT;
@@ -126,21 +126,77 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
   };
   using F = std::integral_constant<bool, false>;
   using T = std::integral_constant<bool, true>;
+  // INC: incremental combine (resident.cuh hop_acc) — the register-only
+  // internal hops are summed before the exchange barrier, the face hops after
+  auto interior = [&](auto dag, const Spinor* v, Spinor* out) {
+    constexpr bool DAG = decltype(dag)::value;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      const int i = k / BT, j = k % BT;
+      bool first = true;
+      if (i < BX - 1) {
+        hop_acc<DAG, 0>(out[k], cmul(u0[k], e0(dag, v[k + BT])), first, v[k], a.diag);
+        first = false;
+      }
+      if (i > 0) {
+        hop_acc<DAG, 1>(out[k], e1(dag, v[k - BT], k - BT), first, v[k], a.diag);
+        first = false;
+      }
+      if (j < BT - 1) {
+        hop_acc<DAG, 2>(out[k], cmul(u1[k], e2(dag, v[k + 1])), first, v[k], a.diag);
+        first = false;
+      }
+      if (j > 0) hop_acc<DAG, 3>(out[k], e3(dag, v[k - 1], k - 1), first, v[k], a.diag);
+    }
+  };
+  auto faces = [&](auto dag, const double2* E, Spinor* out) {
+    constexpr bool DAG = decltype(dag)::value;
+    double2 fx[SPT], ft[SPT];
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      const int i = k / BT, j = k % BT;
+      if (i == BX - 1) fx[k] = E[O0 + j * NT + txp];
+      if (i == 0) fx[k] = E[O1 + j * NT + txm];
+      if (j == BT - 1) ft[k] = E[O2 + i * NT + ttp];
+      if (j == 0) ft[k] = E[O3 + i * NT + ttm];
+    }
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      const int i = k / BT, j = k % BT;
+      if (i == BX - 1) hop_acc<DAG, 0>(out[k], cmul(u0[k], fx[k]), false, out[k], 0.0);
+      if (i == 0) hop_acc<DAG, 1>(out[k], fx[k], false, out[k], 0.0);
+      if (j == BT - 1) hop_acc<DAG, 2>(out[k], cmul(u1[k], ft[k]), false, out[k], 0.0);
+      if (j == 0) hop_acc<DAG, 3>(out[k], ft[k], false, out[k], 0.0);
+    }
+  };
+  static_assert(!INC || (BX >= 2 && BT >= 2), "incremental combine needs internal hops both ways");
 
   // out = D^dag D v (two exchange rounds).  Precondition: every thread has
   // finished reading E0/E1 of the previous application.
   auto normal_op = [&](const Spinor* v, Spinor* out) {
-    Hops h[SPT];
-    produce(F{}, E0, v);
-    __syncthreads();
-    gather(F{}, E0, v, h);
+    if constexpr (INC) {
+      Spinor t[SPT];
+      produce(F{}, E0, v);
+      interior(F{}, v, t);
+      __syncthreads();
+      faces(F{}, E0, t);
+      produce(T{}, E1, t);
+      interior(T{}, t, out);
+      __syncthreads();
+      faces(T{}, E1, out);
+    } else {
+      Hops h[SPT];
+      produce(F{}, E0, v);
+      __syncthreads();
+      gather(F{}, E0, v, h);
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) out[k] = res_combine<false>(h[k], v[k], u0[k], u1[k], a.diag);
-    produce(T{}, E1, out);
-    __syncthreads();
-    gather(T{}, E1, out, h);
+      for (int k = 0; k < SPT; ++k) out[k] = res_combine<false>(h[k], v[k], u0[k], u1[k], a.diag);
+      produce(T{}, E1, out);
+      __syncthreads();
+      gather(T{}, E1, out, h);
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) out[k] = res_combine<true>(h[k], out[k], u0[k], u1[k], a.diag);
+      for (int k = 0; k < SPT; ++k) out[k] = res_combine<true>(h[k], out[k], u0[k], u1[k], a.diag);
+    }
   };
 
   Spinor w[SPT];
@@ -165,23 +221,40 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
   for (int it = 1; it <= a.maxiter; ++it) {
     // w = D^dag D p; <p, D^dag D p> formed as ||D p||^2 during the D stage
     // and published by the barrier between the stages (resident.cuh)
-    Hops h[SPT];
-    produce(F{}, E0, p);
-    __syncthreads();
-    gather(F{}, E0, p, h);
-    double dd = 0.0;
+    if constexpr (INC) {
+      Spinor t[SPT];
+      produce(F{}, E0, p);
+      interior(F{}, p, t);
+      __syncthreads();
+      faces(F{}, E0, t);
+      double dd = 0.0;
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      w[k] = res_combine<false>(h[k], p[k], u0[k], u1[k], a.diag);
-      dd += spinor_norm2(w[k]);
+      for (int k = 0; k < SPT; ++k) dd += spinor_norm2(t[k]);
+      produce(T{}, E1, t);
+      interior(T{}, t, w);
+      dd = warp_sum(dd);
+      if ((tid & 31) == 0) red[0][tid >> 5] = dd;
+      __syncthreads();
+      faces(T{}, E1, w);
+    } else {
+      Hops h[SPT];
+      produce(F{}, E0, p);
+      __syncthreads();
+      gather(F{}, E0, p, h);
+      double dd = 0.0;
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        w[k] = res_combine<false>(h[k], p[k], u0[k], u1[k], a.diag);
+        dd += spinor_norm2(w[k]);
+      }
+      produce(T{}, E1, w);
+      dd = warp_sum(dd);
+      if ((tid & 31) == 0) red[0][tid >> 5] = dd;
+      __syncthreads();
+      gather(T{}, E1, w, h);
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) w[k] = res_combine<true>(h[k], w[k], u0[k], u1[k], a.diag);
     }
-    produce(T{}, E1, w);
-    dd = warp_sum(dd);
-    if ((tid & 31) == 0) red[0][tid >> 5] = dd;
-    __syncthreads();
-    gather(T{}, E1, w, h);
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) w[k] = res_combine<true>(h[k], w[k], u0[k], u1[k], a.diag);
     double den = red[0][0];
 #pragma unroll
     for (int q = 1; q < NW; ++q) den += red[0][q];
