@@ -15,11 +15,16 @@ face exchanges it needs, so the same schedules drive both paths:
 * inner_leapfrog  micro steps with one q exchange after every drift
 * Hamiltonian     own-row sums per strip (sch_dd_own_sum) + a global sum
 
-Supported schemes: leapfrog, 5stage, nested-leapfrog, nested-5stage,
-adapted-nested-fg (the gauge force-gradient pieces of the other four are
-not yet wired for strips).  With host draws scattered from the full-lattice
-reference generator the result equals hmc_update on the whole lattice
-(tests/test_gpu_dd.py).
+* kick_fg_full     gauge force, fermion force, C_GG (plaquettes two rows
+                  out: the 2-row halo), the gauge Hessian dot f and both
+                  fermion Hessian dots (weights g and f, faces refreshed)
+* kick_fg_approx  the force at q shifted along it (shifted links' faces
+                  exchanged, a second chi/xi solve on them)
+* inner_fg        micro 5-stage FG steps of the gauge action
+
+All nine reference schemes run on strips.  With host draws scattered from
+the full-lattice reference generator the result equals hmc_update on the
+whole lattice (tests/test_gpu_dd.py).
 """
 
 from __future__ import annotations
@@ -38,7 +43,8 @@ from .hmc import TrajectoryStats, metropolis
 from .integrators import FG_KICK_SIGN, PROGRAMS, IntegratorSpec
 from .lattice import as_links, as_spinor
 
-SUPPORTED = ("leapfrog", "5stage", "nested-leapfrog", "nested-5stage", "adapted-nested-fg")
+SUPPORTED = ("leapfrog", "5stage", "5stage-fg", "fg-approx", "11stage", "nested-leapfrog",
+             "nested-5stage", "nested-fg", "adapted-nested-fg")
 
 
 def _call(name, *args):
@@ -137,17 +143,42 @@ def _kick_fermion(st: DDState, dt: float, full: bool = False):
     st.p = out
 
 
-def _kick_fg_fermion(st: DDState, b_dt: float, c_dt3: float):
-    if c_dt3 == 0.0:
-        _kick_fermion(st, b_dt)
-        return
-    op, chi, xi = st.solve_pair()
+def _fermion_force(st: DDState, op, chi, xi):
+    """f on every row whose stencil stays inside the strip, faces refreshed
+    (weights are read one row out of the own range)."""
     f = torch.empty_like(st.p)
     _call("sch_fermion_force", _lib.ptr(op.U), _lib.ptr(chi), _lib.ptr(xi), _lib.ptr(f), st.S,
           st.Lext, st.T)
-    st.xlinks(f)                                  # weights one row out of the own range
+    return st.xlinks(f)
+
+
+def _gauge_force(st: DDState, q=None):
+    """beta-scaled gauge force of q (default: the state's links), faces refreshed."""
+    q = st.q if q is None else q
+    g = torch.empty_like(q)
+    _call("sch_gauge_force", _lib.ptr(q), float(st.beta), _lib.ptr(g), st.S, st.Lext, st.T)
+    return st.xlinks(g)
+
+
+def _fg_gauge_gauge(st: DDState):
+    """C_GG: plaquettes up to two rows out of each own row, i.e. the 2-row halo."""
+    out = torch.empty_like(st.q)
+    _call("sch_fg_gauge_gauge", _lib.ptr(st.q), float(st.beta), _lib.ptr(out), st.S, st.Lext, st.T)
+    return out
+
+
+def _gauge_hessian_dot(st: DDState, w):
+    out = torch.empty_like(st.q)
+    _call("sch_gauge_hessian_dot", _lib.ptr(st.q), float(st.beta), _lib.ptr(w), _lib.ptr(out), st.S,
+          st.Lext, st.T)
+    return out
+
+
+def _fermion_hessian_dot(st: DDState, op, chi, xi, weight):
+    """fg_fermion_hessian_dot (fermion.py:397-417) on strips: weighted w-sums,
+    Z1 = D^{-dag} b1, Z2 = D^{-1}(b2 + Z1), contraction; 2 inversions."""
     b1, b2 = torch.empty_like(chi), torch.empty_like(chi)
-    _call("sch_weighted_w_sums", _lib.ptr(op.U), _lib.ptr(f), _lib.ptr(chi), _lib.ptr(xi),
+    _call("sch_weighted_w_sums", _lib.ptr(op.U), _lib.ptr(weight), _lib.ptr(chi), _lib.ptr(xi),
           _lib.ptr(b1), _lib.ptr(b2), st.S, st.Lext, st.T)
     z1 = st.dslash(op, st.cg(op, st.xspin(b1)), False)        # D^{-dag} b1
     st.counter.add(1)
@@ -157,11 +188,75 @@ def _kick_fg_fermion(st: DDState, b_dt: float, c_dt3: float):
     st.counter.add(1)
     fg = torch.empty_like(st.p)
     _call("sch_fg_fermion_combine", _lib.ptr(op.U), _lib.ptr(z1), _lib.ptr(z2), _lib.ptr(chi),
-          _lib.ptr(xi), _lib.ptr(f), _lib.ptr(fg), st.S, st.Lext, st.T)
+          _lib.ptr(xi), _lib.ptr(weight), _lib.ptr(fg), st.S, st.Lext, st.T)
+    return fg
+
+
+def _fg_kick(st: DDState, force, b_dt: float, fg, c_dt3: float):
     out = torch.empty_like(st.p)
-    _call("sch_kick", _lib.ptr(st.p), _lib.ptr(f), float(b_dt), _lib.ptr(fg),
+    _call("sch_kick", _lib.ptr(st.p), _lib.ptr(force), float(b_dt), _lib.ptr(fg),
           float(FG_KICK_SIGN * c_dt3), _lib.ptr(out), st.p.numel())
     st.p = out
+
+
+def _kick_fg_fermion(st: DDState, b_dt: float, c_dt3: float):
+    if c_dt3 == 0.0:
+        _kick_fermion(st, b_dt)
+        return
+    op, chi, xi = st.solve_pair()
+    f = _fermion_force(st, op, chi, xi)
+    _fg_kick(st, f, b_dt, _fermion_hessian_dot(st, op, chi, xi, f), c_dt3)
+
+
+def _kick_fg_full(st: DDState, b_dt: float, c_dt3: float):
+    """integrators.kick_fg_full on strips; 6 inversions."""
+    if c_dt3 == 0.0:
+        _kick_fermion(st, b_dt, full=True)
+        return
+    op, chi, xi = st.solve_pair()
+    f = _fermion_force(st, op, chi, xi)
+    g = _gauge_force(st)
+    fg = ((_fg_gauge_gauge(st) + _gauge_hessian_dot(st, f)) + _fermion_hessian_dot(st, op, chi, xi, g)) \
+        + _fermion_hessian_dot(st, op, chi, xi, f)
+    _fg_kick(st, g + f, b_dt, fg, c_dt3)
+
+
+def _kick_fg_approx(st: DDState, b_dt: float, c_dt3: float):
+    """integrators.kick_fg_approx on strips: the force at q shifted along the
+    force; 4 inversions."""
+    if c_dt3 == 0.0:
+        _kick_fermion(st, b_dt, full=True)
+        return
+    op, chi, xi = st.solve_pair()
+    force = _gauge_force(st) + _fermion_force(st, op, chi, xi)
+    qs = torch.empty_like(st.q)
+    _call("sch_rotate_links", _lib.ptr(st.q), _lib.ptr(force), float(2.0 * FG_KICK_SIGN * c_dt3 / b_dt),
+          _lib.ptr(qs), qs.numel())
+    qs = st.xlinks(qs)
+    op2 = DDWilsonDirac(st.lat, qs, st.m0, st.fermion_bc)
+    xi2 = st.cg(op2, st.eta)
+    chi2 = st.dslash(op2, st.xspin(xi2), False)
+    st.counter.add(2)
+    shifted = _gauge_force(st, qs) + _fermion_force(st, op2, chi2, xi2)
+    _fg_kick(st, shifted, b_dt, None, 0.0)
+
+
+def _kick_fg_gauge(st: DDState, b_dt: float, c_dt3: float):
+    if c_dt3 == 0.0:
+        _kick_gauge(st, b_dt)
+        return
+    _fg_kick(st, _gauge_force(st), b_dt, _fg_gauge_gauge(st), c_dt3)
+
+
+def _inner_fg(st: DDState, span: float, m: int, fgc: float):
+    delta = span / m
+    c_d3 = fgc * delta**3
+    for _ in range(m):
+        _kick_gauge(st, delta / 6.0)
+        _drift(st, 0.5 * delta)
+        _kick_fg_gauge(st, 2.0 * delta / 3.0, c_d3)
+        _drift(st, 0.5 * delta)
+        _kick_gauge(st, delta / 6.0)
 
 
 def _inner_leapfrog(st: DDState, span: float, m: int):
@@ -183,8 +278,14 @@ def _run_program(st: DDState, scheme: str, h: float, m: int, fgc: float):
             _kick_fermion(st, w)
         elif name == "Gfermion":
             _kick_fg_fermion(st, w, fgc * h**3)
+        elif name == "Gfull":
+            _kick_fg_full(st, w, fgc * h**3)
+        elif name == "Gapprox":
+            _kick_fg_approx(st, w, fgc * h**3)
         elif name == "Ileapfrog":
             _inner_leapfrog(st, w, m)
+        elif name == "Ifg":
+            _inner_fg(st, w, m, fgc)
         else:
             raise NotImplementedError(f"{name} in {scheme} is not wired for strips")
 

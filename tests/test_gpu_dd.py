@@ -40,7 +40,10 @@ def test_dd_normal_and_cg_match_single_lattice(L, T, G):
 
 
 @pytest.mark.parametrize("scheme,h,G", [("adapted-nested-fg", 0.25, 4), ("5stage", 0.2, 2),
-                                        ("nested-leapfrog", 0.25, 8)])
+                                        ("nested-leapfrog", 0.25, 8), ("5stage-fg", 0.25, 2),
+                                        ("fg-approx", 0.25, 4), ("11stage", 0.5, 2),
+                                        ("nested-fg", 0.25, 4), ("nested-5stage", 0.25, 2),
+                                        ("leapfrog", 0.125, 4)])
 def test_dd_hmc_update_matches_reference_full_lattice(scheme, h, G):
     """HMC on strips (draws from the full-lattice reference generator) ==
     the oracle's hmc_update on the whole lattice: dH <= 1e-8, same accept
@@ -50,7 +53,7 @@ def test_dd_hmc_update_matches_reference_full_lattice(scheme, h, G):
     from paper_1512_03812_b200.dd_hmc import dd_hmc_update
     from oracle import schwinger_oracle as O
     L = 16
-    kw = dict(L=L, T=L, beta=2.0, m0=0.1, tau=1.0 if scheme != "5stage" else 0.4, h=h,
+    kw = dict(L=L, T=L, beta=2.0, m0=0.1, tau=1.0 if scheme == "adapted-nested-fg" else 0.5, h=h,
               scheme=scheme, micro_per_call=2 if scheme.startswith(("nested", "adapted")) else None,
               cg_tol=1e-10)
     cfg, ocfg = sw.HmcConfig(**kw), O.Config(**kw)
