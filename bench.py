@@ -48,16 +48,16 @@ FALLBACK_HBM = 6650.0
 # The dominant kernel of each ensemble workload, and the DRAM bytes per
 # lattice site of one of its launches measured by ncu --set full (U and b
 # in, x out — the solve itself stays on chip):
-#   cfg3: profiles/r01/ncu_full_k_cg_resblk.txt, 33.590016 MB read + 6.144 KB
+#   cfg3: profiles/r01/ncu_full_k_cg_resblk.txt, 33.589504 MB read + 8.192 KB
 #         written for 2048 chains x 256 sites
 #   cfg4: profiles/r01/ncu_full_k_cg_cluster.txt, 268.8832 MB read +
 #         103.359744 MB written for 1024 chains x 4096 sites (b is re-read by
 #         the true-residual checks; part of it misses L2)
 DRAM_CFG4 = (268.8832e6 + 103.359744e6) / (1024 * 4096)
 CG_KERNELS = {
-    "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread> (per-chain CG, one 64-thread CTA "
-                        "per chain, 4 CTAs/SM)",
-                 dram_per_site=(33.590016e6 + 6.144e3) / (2048 * 256),
+    "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread,incremental> (per-chain CG, one "
+                        "64-thread CTA per chain, 4 CTAs/SM)",
+                 dram_per_site=(33.589504e6 + 8.192e3) / (2048 * 256),
                  source="profiles/r01/ncu_full_k_cg_resblk.txt"),
     "cfg4": dict(kernel="k_cg_cluster_tx<64,64,4 CTAs,2x2 sites/thread> (per-chain CG, one "
                         "4-CTA cluster per chain, faces and partial sums pushed with st.async "
