@@ -79,6 +79,11 @@ int sch_avg_plaquette(sch_ctx* ctx, const double* q, double* out, int B, int L, 
 /* C_GG closed form (gauge.py:97-107) */
 int sch_fg_gauge_gauge(sch_ctx* ctx, const double* q, double beta, double* out, int B, int L, int T);
 /* 2 * sum w * Hess(S_G) (gauge.py:110-136) */
+/* gauge.oriented_plaquettes (K = 1, out (B,2,L,T) c128) and
+ * gauge.plaquette_stencil (K = 8, out (8,B,2,L,T) c128): the mu-oriented
+ * plaquette P1 and its translates P2..P8 attached to link (n,mu)
+ * (pkg/src/schwinger/gauge.py:62-95) */
+int sch_plaquette_stencil(sch_ctx* ctx, const double* q, double* out, int K, int B, int L, int T);
 int sch_gauge_hessian_dot(sch_ctx* ctx, const double* q, double beta, const double* w,
                           double* out, int B, int L, int T);
 
@@ -118,6 +123,10 @@ int sch_cg_normal(sch_ctx* ctx, const double* U, const double* b, double* x, con
  * kick_full, integrators.py:172-186) */
 int sch_fermion_force(sch_ctx* ctx, const double* U, const double* chi, const double* xi,
                       double* out, int B, int L, int T);
+/* fermion.link_bilinears(op, mu, a, b) (pkg/src/schwinger/fermion.py:317-327):
+ * A, Bout (B,L,T) c128 */
+int sch_link_bilinears(sch_ctx* ctx, const double* U, const double* a, const double* b, int mu,
+                       double* A, double* Bout, int B, int L, int T);
 int sch_kick_fermion(sch_ctx* ctx, const double* U, const double* chi, const double* xi,
                      const double* q, double beta, const double* p, double dt, double* p_out,
                      int B, int L, int T);

@@ -161,6 +161,32 @@ def _oriented_plaquette(q, mu):
     return z if mu == 0 else np.conj(z)
 
 
+def oriented_plaquettes(q):
+    """P1(n, mu) stacked over mu, shape (..., 2, L, T) (gauge.py:62-67)."""
+    return np.stack([_oriented_plaquette(q, 0), _oriented_plaquette(q, 1)], axis=-3)
+
+
+def plaquette_stencil(q):
+    """The eight translates P1..P8 of the mu-oriented plaquette attached to
+    link (n, mu), shape (8, ..., 2, L, T) (gauge.py:70-95):
+    P2 = P1(n-nu), P3 = P1(n+mu), P4 = P1(n+nu), P5 = P1(n-mu),
+    P6 = P1(n-mu-nu), P7 = P1(n-2nu), P8 = P1(n+mu-nu)."""
+    p1 = oriented_plaquettes(q)
+    out = np.empty((8,) + p1.shape, dtype=p1.dtype)
+    for mu in (0, 1):
+        nu = 1 - mu
+        base = p1[..., mu, :, :]
+        out[0, ..., mu, :, :] = base
+        out[1, ..., mu, :, :] = at_bwd(base, nu)
+        out[2, ..., mu, :, :] = at_fwd(base, mu)
+        out[3, ..., mu, :, :] = at_fwd(base, nu)
+        out[4, ..., mu, :, :] = at_bwd(base, mu)
+        out[5, ..., mu, :, :] = at_bwd(at_bwd(base, mu), nu)
+        out[6, ..., mu, :, :] = at_bwd(base, nu, 2)
+        out[7, ..., mu, :, :] = at_bwd(at_fwd(base, mu), nu)
+    return out
+
+
 def fg_gauge_gauge(q, beta):
     """Closed-form C_GG from the eight translated plaquettes
     (gauge.py:70-107)."""
@@ -415,6 +441,11 @@ def _bilinears(U, mu, a, b):
     A_ = np.conj(_w(a0, a1, mu, -1)) * u * at_fwd(_w(b0, b1, mu, -1), mu)
     B_ = np.conj(at_fwd(_w(a0, a1, mu, +1), mu)) * np.conj(u) * _w(b0, b1, mu, +1)
     return A_, B_
+
+
+def link_bilinears(U, mu, a, b):
+    """(A, B) hopping contractions attached to link (n, mu) (fermion.py:317-327)."""
+    return _bilinears(U, mu, a, b)
 
 
 def fermion_force(U, chi, xi):

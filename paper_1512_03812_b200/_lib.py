@@ -43,6 +43,9 @@ _SIGNATURES = {
     "sch_avg_plaquette": [_c_ptr, _c_ptr, _c_ptr, _c_int, _c_int, _c_int],
     "sch_fg_gauge_gauge": [_c_ptr, _c_ptr, _c_dbl, _c_ptr, _c_int, _c_int, _c_int],
     "sch_gauge_hessian_dot": [_c_ptr, _c_ptr, _c_dbl, _c_ptr, _c_ptr, _c_int, _c_int, _c_int],
+    "sch_plaquette_stencil": [_c_ptr, _c_ptr, _c_ptr, _c_int, _c_int, _c_int, _c_int],
+    "sch_link_bilinears": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_int, _c_ptr, _c_ptr, _c_int, _c_int,
+                           _c_int],
     "sch_links_to_u": [_c_ptr, _c_ptr, _c_ptr, _c_int, _c_int, _c_int, _c_int],
     "sch_dslash": [_c_ptr, _c_ptr, _c_int, _c_ptr, _c_ptr, _c_int, _c_int, _c_int, _c_dbl, _c_int],
     "sch_ddagd": [_c_ptr, _c_ptr, _c_ptr, _c_ptr, _c_int, _c_int, _c_int, _c_dbl],

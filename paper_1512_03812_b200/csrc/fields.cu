@@ -179,6 +179,35 @@ __global__ void k_fg_gauge_gauge(const double* __restrict__ q, double beta, doub
   }
 }
 
+// The mu-oriented plaquettes P1(n, mu) = e^{+-i theta} and (K = 8) their
+// seven translates P2..P8 attached to link (n, mu) (gauge.py:62-95), as
+// complex fields out[k][b][mu][x][t].
+__global__ void k_plaquette_stencil(const double* __restrict__ q, double2* __restrict__ out, int K,
+                                    Geo g) {
+  long long n = (long long)g.B * g.V;
+  const long long plane = (long long)g.B * 2 * g.V;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    int b = (int)(i / g.V);
+    int s = (int)(i - (long long)b * g.V);
+    int x = s / g.T, t = s - x * g.T;
+    const double* qc = q + (long long)b * 2 * g.V;
+    for (int mu = 0; mu < 2; ++mu) {
+      const int mx = mu == 0, mt = mu == 1, nx = mu == 1, nt = mu == 0;
+      const int ox[8] = {0, -nx, mx, nx, -mx, -mx - nx, -2 * nx, mx - nx};
+      const int ot[8] = {0, -nt, mt, nt, -mt, -mt - nt, -2 * nt, mt - nt};
+      for (int k = 0; k < K; ++k) {
+        int xx = x + ox[k], tt = t + ot[k];
+        xx = xx < 0 ? xx + g.L : (xx >= g.L ? xx - g.L : xx);
+        tt = tt < 0 ? tt + g.T : (tt >= g.T ? tt - g.T : tt);
+        double sn, cs;
+        sincos(plaq(qc, g.L, g.T, xx, tt), &sn, &cs);
+        out[k * plane + (long long)b * 2 * g.V + mu * g.V + s] = make_double2(cs, mu == 0 ? sn : -sn);
+      }
+    }
+  }
+}
+
 // 2*beta*[(w(n,mu)+w(n+mu,nu)-w(n+nu,mu)-w(n,nu)) Re P1
 //        +(w(n,mu)-w(n+mu-nu,nu)-w(n-nu,mu)+w(n-nu,nu)) Re P2]   (gauge.py:110-136)
 __global__ void k_gauge_hessian_dot(const double* __restrict__ q, double beta,
@@ -409,6 +438,15 @@ int sch_fg_gauge_gauge(sch_ctx* ctx, const double* q, double beta, double* out, 
   SCH_CHECK_ARG(ctx, q && out && B >= 1 && L >= 2 && T >= 2, "fg_gauge_gauge: bad args");
   Geo g{B, L, T, (long long)L * T};
   k_fg_gauge_gauge<<<grid_for((long long)B * g.V), 256, 0, ctx->stream>>>(q, beta, out, g);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+int sch_plaquette_stencil(sch_ctx* ctx, const double* q, double* out, int K, int B, int L, int T) {
+  SCH_CHECK_ARG(ctx, q && out && (K == 1 || K == 8) && B >= 1 && L >= 2 && T >= 2,
+                "plaquette_stencil: bad args");
+  Geo g{B, L, T, (long long)L * T};
+  k_plaquette_stencil<<<grid_for((long long)B * g.V), 256, 0, ctx->stream>>>(q, (double2*)out, K, g);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }

@@ -164,6 +164,29 @@ __global__ void k_fermion_force(const double2* __restrict__ U, const double2* __
   }
 }
 
+// The two hopping contractions of link (n, mu) as fields (fermion.py:317-327):
+// A(n) = conj(w-(a)(n)) U_mu(n) w-(b)(n+mu), B(n) = conj(w+(a)(n+mu)) conj(U_mu(n)) w+(b)(n),
+// products evaluated left to right as NumPy does.
+__global__ void k_link_bilinears(const double2* __restrict__ U, const double2* __restrict__ a,
+                                 const double2* __restrict__ bv, int mu, double2* __restrict__ outA,
+                                 double2* __restrict__ outB, Geo g) {
+  long long n = (long long)g.B * g.V;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long b = i / g.V;
+    int s = (int)(i - b * g.V);
+    int x = s / g.T, t = s - x * g.T;
+    int f = mu == 0 ? (x + 1 == g.L ? 0 : x + 1) * g.T + t : x * g.T + (t + 1 == g.T ? 0 : t + 1);
+    long long cb = b * g.V;
+    Spinor an = ld256_spinor_nc(a, cb + s), af = ld256_spinor_nc(a, cb + f);
+    Spinor bn = ld256_spinor_nc(bv, cb + s), bf = ld256_spinor_nc(bv, cb + f);
+    double2 u = __ldg(U + 2 * cb + (long long)mu * g.V + s);
+    Bil r = mu == 0 ? bilinear<0>(an, af, bn, bf, u) : bilinear<1>(an, af, bn, bf, u);
+    outA[cb + s] = r.A;
+    outB[cb + s] = r.B;
+  }
+}
+
 // Weighted w-sums (fermion.py:362-383, Appendix A5), gather form per site.
 __global__ void k_wsums(const double2* __restrict__ U, const double* __restrict__ wt,
                         const double2* __restrict__ chi, const double2* __restrict__ xi,
@@ -334,6 +357,17 @@ int sch_fermion_force(sch_ctx* ctx, const double* U, const double* chi, const do
   Geo g{B, L, T, (long long)L * T};
   k_fermion_force<false><<<grid_for((long long)B * g.V), 256, 0, ctx->stream>>>(
       (const double2*)U, (const double2*)chi, (const double2*)xi, nullptr, 0.0, nullptr, 0.0, out, g);
+  SCH_LAUNCHED(ctx);
+  return SCH_OK;
+}
+
+int sch_link_bilinears(sch_ctx* ctx, const double* U, const double* a, const double* b, int mu,
+                       double* A, double* Bout, int B, int L, int T) {
+  SCH_CHECK_ARG(ctx, U && a && b && A && Bout && (mu == 0 || mu == 1) && B >= 1 && L >= 2 && T >= 2,
+                "link_bilinears: bad args");
+  Geo g{B, L, T, (long long)L * T};
+  k_link_bilinears<<<grid_for((long long)B * g.V), 256, 0, ctx->stream>>>(
+      (const double2*)U, (const double2*)a, (const double2*)b, mu, (double2*)A, (double2*)Bout, g);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }

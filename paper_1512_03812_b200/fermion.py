@@ -391,6 +391,21 @@ def _spinors(op, *fields):
     return [f.expand(shape).contiguous() if f.shape != shape else f for f in out]
 
 
+def link_bilinears(op: WilsonDirac, mu: int, a, b):
+    """The two hopping contractions attached to link (n, mu) (fermion.py:317-327):
+    A(n) = a(n)^dag (1 - s_mu) U_mu(n) b(n + mu), B(n) = a(n + mu)^dag (1 + s_mu) U*_mu(n) b(n),
+    as complex fields of shape a.shape[:-1]; kernel k_link_bilinears."""
+    if mu not in (0, 1):
+        raise ValueError(f"direction must be 0 or 1, got {mu}")
+    a, b = _spinors(op, a, b)
+    U = op._U_for(tuple(a.shape[:-3]))
+    A = torch.empty(a.shape[:-1], dtype=torch.complex128, device=a.device)
+    Bv = torch.empty_like(A)
+    _lib.ctx().call("sch_link_bilinears", _lib.ptr(U), _lib.ptr(a), _lib.ptr(b), int(mu), _lib.ptr(A),
+                    _lib.ptr(Bv), n_chains(a), op.L, op.T)
+    return A, Bv
+
+
 def fermion_force(op: WilsonDirac, chi, xi) -> torch.Tensor:
     """f(n,mu) = -Im[A - B] (fermion.py:330-336); kernel k_fermion_force."""
     chi, xi = _spinors(op, chi, xi)

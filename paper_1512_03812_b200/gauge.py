@@ -25,6 +25,29 @@ def plaq_angles(q) -> torch.Tensor:
     return out
 
 
+def _plaquette_stencil(q, K: int) -> torch.Tensor:
+    q = as_links(q)
+    B, L, T = _geo(q)
+    out = torch.empty(((K,) if K > 1 else ()) + tuple(q.shape), dtype=torch.complex128,
+                      device=q.device)
+    _lib.ctx().call("sch_plaquette_stencil", _lib.ptr(q), _lib.ptr(out), K, B, L, T)
+    return out
+
+
+def oriented_plaquettes(q) -> torch.Tensor:
+    """P1(n, mu): the plaquette traversed starting along mu — e^{i theta} for
+    mu=0, its conjugate for mu=1 — shape (..., 2, L, T) (gauge.py:62-67)."""
+    return _plaquette_stencil(q, 1)
+
+
+def plaquette_stencil(q) -> torch.Tensor:
+    """The eight translates P1..P8 of the mu-oriented plaquette attached to
+    link (n, mu), shape (8, ..., 2, L, T) (gauge.py:70-95):
+    P2 = P1(n-nu), P3 = P1(n+mu), P4 = P1(n+nu), P5 = P1(n-mu),
+    P6 = P1(n-mu-nu), P7 = P1(n-2nu), P8 = P1(n-nu+mu)."""
+    return _plaquette_stencil(q, 8)
+
+
 def plaquettes(q) -> torch.Tensor:
     """exp(i * plaquette angle) (gauge.py:27-29), via the sincos link-cache kernel."""
     th = plaq_angles(q)

@@ -174,6 +174,27 @@ def force_cases():
     np.savez_compressed(HERE / "forces.npz", **out)
 
 
+def piece_cases():
+    """Building blocks of the force / force-gradient terms (fermion.py:317-327,
+    gauge.py:62-95): link bilinears for both directions, the oriented
+    plaquettes and the eight-plaquette stencil; unbatched and batched."""
+    out = {}
+    for tag, B in (("u", None), ("b", 3)):
+        rng = sw.make_rng(777, 0 if B is None else 1)
+        L, T = 6, 10
+        lshape = (2, L, T) if B is None else (B, 2, L, T)
+        sshape = (L, T, 2) if B is None else (B, L, T, 2)
+        q = rng.uniform(-np.pi, np.pi, lshape)
+        a, b = cspinor(rng, sshape), cspinor(rng, sshape)
+        op = F.WilsonDirac(q, 0.1)
+        for mu in (0, 1):
+            A, Bb = F.link_bilinears(op, mu, a, b)
+            out[f"{tag}_A{mu}"], out[f"{tag}_B{mu}"] = A, Bb
+        out.update({f"{tag}_q": q, f"{tag}_a": a, f"{tag}_b": b,
+                    f"{tag}_P": G.oriented_plaquettes(q), f"{tag}_stencil": G.plaquette_stencil(q)})
+    np.savez_compressed(HERE / "pieces.npz", **out)
+
+
 def run_chain(q, cfg, rng, n):
     dh, acc, inv, qs = [], [], [], []
     for _ in range(n):
@@ -247,7 +268,7 @@ def therm_fixture():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["stencil", "cg", "force", "traj", "measure", "therm"]
+    which = sys.argv[1:] or ["stencil", "cg", "force", "pieces", "traj", "measure", "therm"]
     for w in which:
-        dict(stencil=stencil_cases, cg=cg_cases, force=force_cases, traj=traj_cases,
-             measure=measure_cases, therm=therm_fixture)[w]()
+        dict(stencil=stencil_cases, cg=cg_cases, force=force_cases, pieces=piece_cases,
+             traj=traj_cases, measure=measure_cases, therm=therm_fixture)[w]()

@@ -196,6 +196,24 @@ def test_cg_cluster_engine_matches_oracle(sw, m0):
 
 
 @pytest.mark.parametrize("tag", ["u", "b"])
+def test_force_pieces_match_reference(sw, golden, tag):
+    """link_bilinears (both directions), oriented_plaquettes, plaquette_stencil
+    against the reference's own outputs (tests/golden/pieces.npz)."""
+    g = golden("pieces")
+    op = sw.WilsonDirac(g[f"{tag}_q"], 0.1)
+    for mu in (0, 1):
+        A, B = sw.link_bilinears(op, mu, g[f"{tag}_a"], g[f"{tag}_b"])
+        assert A.shape == g[f"{tag}_A{mu}"].shape
+        assert rel_err(npy(A), g[f"{tag}_A{mu}"]) < TOL_OP
+        assert rel_err(npy(B), g[f"{tag}_B{mu}"]) < TOL_OP
+    P = sw.oriented_plaquettes(g[f"{tag}_q"])
+    st = sw.plaquette_stencil(g[f"{tag}_q"])
+    assert P.shape == g[f"{tag}_P"].shape and st.shape == g[f"{tag}_stencil"].shape
+    assert rel_err(npy(P), g[f"{tag}_P"]) < TOL_OP
+    assert rel_err(npy(st), g[f"{tag}_stencil"]) < TOL_OP
+
+
+@pytest.mark.parametrize("tag", ["u", "b"])
 def test_forces_match_reference(sw, golden, tag):
     g = golden("forces")
     q, eta, p = g[f"{tag}_q"], g[f"{tag}_eta"], g[f"{tag}_p"]

@@ -107,6 +107,19 @@ def test_oracle_forces_match_reference(golden, tag):
     assert rel_err(sf, g[f"{tag}_SF"]) < 1e-12
 
 
+@pytest.mark.parametrize("tag", ["u", "b"])
+def test_oracle_force_pieces_match_reference(golden, tag):
+    """link_bilinears (both mu), oriented_plaquettes, plaquette_stencil."""
+    g = golden("pieces")
+    U = O.fermion_links(g[f"{tag}_q"])
+    for mu in (0, 1):
+        A, B = O.link_bilinears(U, mu, g[f"{tag}_a"], g[f"{tag}_b"])
+        assert rel_err(A, g[f"{tag}_A{mu}"]) < 1e-14
+        assert rel_err(B, g[f"{tag}_B{mu}"]) < 1e-14
+    assert rel_err(O.oriented_plaquettes(g[f"{tag}_q"]), g[f"{tag}_P"]) < 1e-14
+    assert rel_err(O.plaquette_stencil(g[f"{tag}_q"]), g[f"{tag}_stencil"]) < 1e-14
+
+
 def test_oracle_measure_dh_matches_reference(golden):
     g = golden("measure")
     for k, scheme in enumerate(("adapted-nested-fg", "5stage-fg", "leapfrog")):
