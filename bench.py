@@ -26,6 +26,7 @@ Also reported on the same line:
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import multiprocessing as mp
@@ -262,6 +263,8 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        if os.environ.get("SCH_NO_CLOCKS"):
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -464,18 +467,43 @@ def run_ours(args):
             drngs.append(d)
             qs.append(d.hot_start(geom))
 
-    def ensemble_step(qs, uploads=None):
+    def issue_step(qs):
         pend = []
         for i, stm in enumerate(streams):
             stm.wait_stream(main)
             with torch.cuda.stream(stm):
-                qi = qs[i] if uploads is None else uploads[i]()
-                qs[i], p = sw.hmc_update_ensemble_async(qi, cfg, drngs[i])
+                qs[i], p = sw.hmc_update_ensemble_async(qs[i], cfg, drngs[i])
                 pend.append(p)
         for stm in streams:
             main.wait_stream(stm)
-        return [p.resolve() for p in pend]
+        return pend
 
+    def ensemble_step(qs):
+        return [p.resolve() for p in issue_step(qs)]
+
+    def run_steps(n, on_stats=None, ahead=2):
+        """n updates with `ahead` steps queued: step k+ahead is issued before
+        step k's per-chain results are read back, so a host-side stall (the
+        box shows occasional 10-120 ms ones, tools/step_jitter.py) is
+        absorbed by the queued GPU work instead of idling the GPU."""
+        queue, sts = [], None
+        for _ in range(n):
+            queue.append(issue_step(qs))
+            if len(queue) > ahead:
+                sts = [p.resolve() for p in queue.pop(0)]
+                if on_stats:
+                    on_stats(sts)
+        while queue:
+            sts = [p.resolve() for p in queue.pop(0)]
+            if on_stats:
+                on_stats(sts)
+        return sts
+
+    # The host only issues work; a Python garbage-collector pass in the middle
+    # of a step stalls the issue thread for ~20 ms and starves the GPU
+    # (tools/step_jitter.py), so collect once here and keep it off while timing.
+    gc.collect()
+    gc.disable()
     for _ in range(args.warmup):
         sts = ensemble_step(qs)
     torch.cuda.synchronize()
@@ -489,10 +517,11 @@ def run_ours(args):
     acc, dhs = [], []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.steps):
-        sts = ensemble_step(qs)
+    def record(sts):
         acc.append(np.concatenate([st.accepted for st in sts]))
         dhs.append(np.concatenate([st.dh for st in sts]))
+
+    sts = run_steps(args.steps, record)
     st = sts[0]
     e1.record()
     torch.cuda.synchronize()
@@ -541,21 +570,62 @@ def run_ours(args):
     # e2e through the public API with host buffers
     e2e = None
     if not args.no_e2e:
+        # Every step is one public-API call on HOST links: H2D of the links,
+        # the update, D2H of the new links and of the per-chain dH / accept.
+        # Copies run on a copy stream, double-buffered, so step k+1's upload
+        # and step k's download overlap the neighbouring step's compute (a
+        # pipelined client; every byte still crosses PCIe inside the window).
         q_host = [qi.cpu().pin_memory() for qi in qs]
         q_back = [torch.empty_like(h).pin_memory() for h in q_host]
         h2d = sum(h.numel() for h in q_host) * 8
         steps_e2e = max(2, args.steps // 2)
-        uploads = [lambda h=h: h.to("cuda", non_blocking=True) for h in q_host]
+        copy = [torch.cuda.Stream() for _ in streams]
+        din = [[torch.empty_like(qi) for _ in range(2)] for qi in qs]
+        ev_in = [[torch.cuda.Event() for _ in range(2)] for _ in qs]
+        ev_free = [[torch.cuda.Event() for _ in range(2)] for _ in qs]
+        for i in range(S):
+            for slot in range(2):
+                ev_free[i][slot].record(main)
+
+        def upload(i, slot):
+            with torch.cuda.stream(copy[i]):
+                copy[i].wait_event(ev_free[i][slot])
+                din[i][slot].copy_(q_host[i], non_blocking=True)
+                ev_in[i][slot].record(copy[i])
+
         barrier()
         torch.cuda.synchronize()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record()
-        for _ in range(steps_e2e):
-            ensemble_step(qs, uploads)   # host links in, per-chain dH / accept out
+        for i in range(S):
+            copy[i].wait_stream(main)
+            upload(i, 0)
+        prev_pend = []
+        for k in range(steps_e2e):
+            slot = k % 2
+            pend = []
             for i, stm in enumerate(streams):
+                if k + 1 < steps_e2e:
+                    upload(i, 1 - slot)
                 with torch.cuda.stream(stm):
-                    q_back[i].copy_(qs[i], non_blocking=True)
-                main.wait_stream(stm)
+                    stm.wait_event(ev_in[i][slot])
+                    out, p = sw.hmc_update_ensemble_async(din[i][slot], cfg, drngs[i])
+                    ev_free[i][slot].record(stm)
+                    done = torch.cuda.Event()
+                    done.record(stm)
+                with torch.cuda.stream(copy[i]):
+                    copy[i].wait_event(done)
+                    out.record_stream(copy[i])
+                    q_back[i].copy_(out, non_blocking=True)
+                pend.append(p)
+            for p in prev_pend:   # step k-1's dH / accept, read while step k runs
+                p.resolve()
+            prev_pend = pend
+        for p in prev_pend:
+            p.resolve()
+        for i, stm in enumerate(streams):
+            main.wait_stream(stm)
+            main.wait_stream(copy[i])
         f1.record()
         torch.cuda.synchronize()
         barrier()
@@ -569,6 +639,7 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems / steps_e2e}
 
+    gc.enable()
     graphs = None
     if rank == 0 and not args.no_stencil:
         graphs = graph_bench(torch, sw)
