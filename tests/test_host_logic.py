@@ -75,3 +75,35 @@ def test_config_rejects_unknown_keys():
 def test_desk_scale():
     d = C.desk_scale(C.HmcConfig())
     assert (d.L, d.T, d.n_samples, d.n_thermalize) == (8, 8, 50, 200)
+
+
+def test_captured_update_rejects_host_streams_before_touching_the_device():
+    """EnsembleUpdateGraph needs the device-resident NumPy streams (checked
+    before any CUDA work, so this runs without a GPU)."""
+    import paper_1512_03812_b200 as sw
+    cfg = sw.HmcConfig(L=8, T=8)
+    with pytest.raises(TypeError):
+        sw.EnsembleUpdateGraph(None, cfg, device_rng=object())
+
+
+def test_dd_supports_every_reference_scheme():
+    from paper_1512_03812_b200.dd_hmc import SUPPORTED
+    from paper_1512_03812_b200.integrators import PROGRAMS, SCHEME_IDS
+    assert set(SUPPORTED) == set(SCHEME_IDS)
+    wired = {"D", "K", "Kf", "Gfermion", "Gfull", "Gapprox", "Ileapfrog", "Ifg"}
+    for scheme in SCHEME_IDS:
+        assert {name for name, _ in PROGRAMS[scheme]} <= wired, scheme
+
+
+def test_bench_workload_labels_follow_the_workload():
+    import importlib
+    import sys
+    sys.argv = ["bench.py", "--workload", "cfg4"]
+    bench = importlib.import_module("bench")
+    args = bench.parse()
+    label = bench._phys_label(args.outer)
+    assert label.startswith("64x64 chains") and "m0=0.02" in label and "8x4 steps" in label
+    assert bench.CG_KERNELS["cfg4"]["kernel"].startswith("k_cg_cluster_tx")
+    sys.argv = ["bench.py"]
+    args = bench.parse()
+    assert bench._phys_label(args.outer).startswith("16x16 chains")
