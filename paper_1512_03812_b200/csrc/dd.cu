@@ -183,7 +183,7 @@ struct DDState {
   double* sc;   // scalars: see SC_* below
   int* flag;    // [S] need_x (X pass) per local strip (all equal)
   double* beta; // [S] beta per local strip (all equal)
-  int* ctl;     // [0] done, [1] iters, [2] status
+  int* ctl;     // [0] done, [1] iters, [2] status, [3] current iteration (device-side loop)
 };
 enum { SC_NORMB2 = 0, SC_PAP, SC_RR, SC_TN2, SC_RS, SC_RSNEW, SC_ALPHA, SC_NORMB, SC_TARGET,
        SC_BEST, SC_RELRES, SC_COUNT };
@@ -236,6 +236,14 @@ __global__ void k_dd_ctrl_init(DDState st, int S, double tol, int have_x0) {
   st.ctl[0] = nb == 0.0 ? 1 : 0;   // zero rhs: x = 0, 0 iterations (fermion.py:181-182)
   st.ctl[1] = 0;
   st.ctl[2] = 0;
+  st.ctl[3] = 1;
+}
+
+__global__ void k_dd_iter_inc(DDState st) { ++st.ctl[3]; }
+
+// tail of the device-side loop body: iterate while not done (and below the cap)
+__global__ void k_dd_set_continue(DDState st, int maxiter, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, (st.ctl[0] == 0 && st.ctl[3] <= maxiter) ? 1u : 0u);
 }
 
 __global__ void k_dd_alpha(DDState st) {
@@ -247,9 +255,10 @@ __global__ void k_dd_alpha(DDState st) {
 // p = r + beta p, x += alpha p on every row; r -= alpha ap and ||r||^2 on own rows
 __global__ void k_dd_update(double2* __restrict__ r, double2* __restrict__ p, double2* __restrict__ x,
                             const double2* __restrict__ ap, DDState st, long long nsites, int T, int Lext,
-                            int lo, int hi, int repl, double* __restrict__ part) {
+                            int lo, int hi, double* __restrict__ part) {
   __shared__ double slot[32];
   if (st.ctl[0]) return;
+  const int repl = (st.ctl[3] % kDDReplace) == 0;
   const double al = st.sc[SC_ALPHA], be = st.beta[0];
   double acc = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nsites;
@@ -269,8 +278,9 @@ __global__ void k_dd_update(double2* __restrict__ r, double2* __restrict__ p, do
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-__global__ void k_dd_check(DDState st, int S, int repl) {
+__global__ void k_dd_check(DDState st, int S) {
   if (st.ctl[0]) return;
+  const int repl = (st.ctl[3] % kDDReplace) == 0;
   int need;
   if (repl) {
     need = 1;
@@ -282,8 +292,9 @@ __global__ void k_dd_check(DDState st, int S, int repl) {
   for (int s = 0; s < S; ++s) st.flag[s] = need;
 }
 
-__global__ void k_dd_final(DDState st, int S, int it, int maxiter) {
+__global__ void k_dd_final(DDState st, int S, int maxiter) {
   if (st.ctl[0]) return;
+  const int it = st.ctl[3];
   const int nx = st.flag[0];
   double rs_new = st.sc[SC_RSNEW];
   if (nx) {
@@ -551,34 +562,83 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   txx.flag = st.flag;
   txx.partial = part_b;
 
-  int it = 1, chunk = 4;
-  while (it <= maxiter) {
-    const int n = std::min(chunk, maxiter - it + 1);
-    for (int j = 0; j < n; ++j, ++it) {
-      const int repl = (it % kDDReplace) == 0;
-      if ((rc = dd_exchange(ctx, dd, (double*)r, 1, 4))) return rc;
-      launch_normal_tile<MODE_P>(sh, tp, s);
-      SCH_LAUNCHED(ctx);
-      if ((rc = dd_allsum(ctx, dd, part_a, ntile_part, st.sc + SC_PAP))) return rc;
-      k_dd_alpha<<<1, 1, 0, s>>>(st);
-      SCH_LAUNCHED(ctx);
-      k_dd_update<<<egrid, 256, 0, s>>>(r, p, (double2*)x_ext, ap, st, nsites, dd->T, dd->Lext, lo,
-                                        hi, repl, part_b);
-      SCH_LAUNCHED(ctx);
-      if ((rc = dd_allsum(ctx, dd, part_b, egrid, st.sc + SC_RR))) return rc;
-      k_dd_check<<<1, 1, 0, s>>>(st, dd->S, repl);
-      SCH_LAUNCHED(ctx);
+  // One iteration; the iteration number lives on the device (ctl[3]), so the
+  // body is the same every time and can be captured.
+  auto iteration = [&](cudaStream_t q) -> int {
+    const cudaStream_t saved = ctx->stream;
+    ctx->stream = q;   // dd_exchange / dd_allsum enqueue on ctx->stream
+    int e = SCH_OK;
+    do {
+      if ((e = dd_exchange(ctx, dd, (double*)r, 1, 4))) break;
+      launch_normal_tile<MODE_P>(sh, tp, q);
+      ctx->launches++;
+      if ((e = dd_allsum(ctx, dd, part_a, ntile_part, st.sc + SC_PAP))) break;
+      k_dd_alpha<<<1, 1, 0, q>>>(st);
+      k_dd_update<<<egrid, 256, 0, q>>>(r, p, (double2*)x_ext, ap, st, nsites, dd->T, dd->Lext, lo,
+                                        hi, part_b);
+      ctx->launches += 2;
+      if ((e = dd_allsum(ctx, dd, part_b, egrid, st.sc + SC_RR))) break;
+      k_dd_check<<<1, 1, 0, q>>>(st, dd->S);
       // x halos are current (x is updated on every row), so no exchange here
-      launch_normal_tile<MODE_X>(sh, txx, s);
-      SCH_LAUNCHED(ctx);
-      if ((rc = dd_allsum(ctx, dd, part_b, ntile_part, st.sc + SC_TN2))) return rc;
-      k_dd_final<<<1, 1, 0, s>>>(st, dd->S, it, maxiter);
-      SCH_LAUNCHED(ctx);
+      launch_normal_tile<MODE_X>(sh, txx, q);
+      ctx->launches += 2;
+      if ((e = dd_allsum(ctx, dd, part_b, ntile_part, st.sc + SC_TN2))) break;
+      k_dd_final<<<1, 1, 0, q>>>(st, dd->S, maxiter);
+      k_dd_iter_inc<<<1, 1, 0, q>>>(st);
+      ctx->launches += 2;
+      cudaError_t le = cudaGetLastError();
+      if (le != cudaSuccess) e = sch_fail(ctx, SCH_ERR_CUDA, "dd cg launch: %s", cudaGetErrorString(le));
+    } while (0);
+    ctx->stream = saved;
+    return e;
+  };
+
+  if (dd->comm == nullptr && use_cg_graph() && use_cg_while()) {
+    // local transport: the whole loop on the device (conditional WHILE graph
+    // node, as the streaming engine in cg.cu); NCCL transports keep the
+    // host-driven loop below
+    if (!ctx->cap_stream)
+      SCH_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    cudaGraph_t graph;
+    SCH_CUDA(ctx, cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle handle;
+    SCH_CUDA(ctx, cudaGraphConditionalHandleCreate(&handle, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = handle;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    SCH_CUDA(ctx, cudaGraphAddNode(&cnode, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    SCH_CUDA(ctx, cudaStreamBeginCaptureToGraph(ctx->cap_stream, body, nullptr, nullptr, 0,
+                                                cudaStreamCaptureModeRelaxed));
+    int e = iteration(ctx->cap_stream);
+    k_dd_set_continue<<<1, 1, 0, ctx->cap_stream>>>(st, maxiter, handle);
+    cudaGraph_t captured;
+    cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &captured);
+    if (e || ce != cudaSuccess) {
+      cudaGraphDestroy(graph);
+      return e ? e : sch_fail(ctx, SCH_ERR_CUDA, "dd cg capture: %s", cudaGetErrorString(ce));
     }
-    SCH_CUDA(ctx, cudaMemcpyAsync(ctx->h_flag, st.ctl, sizeof(int), cudaMemcpyDeviceToHost, s));
-    SCH_CUDA(ctx, cudaStreamSynchronize(s));
-    if (*ctx->h_flag) break;
-    chunk = std::min(chunk * 2, 32);
+    cudaGraphExec_t exec;
+    cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "dd cg instantiate: %s", cudaGetErrorString(ie));
+    cudaError_t le = cudaGraphLaunch(exec, s);
+    cudaGraphExecDestroy(exec);
+    if (le != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "dd cg graph launch: %s", cudaGetErrorString(le));
+  } else {
+    int it = 1, chunk = 4;
+    while (it <= maxiter) {
+      const int n = std::min(chunk, maxiter - it + 1);
+      for (int j = 0; j < n; ++j, ++it)
+        if ((rc = iteration(s))) return rc;
+      SCH_CUDA(ctx, cudaMemcpyAsync(ctx->h_flag, st.ctl, sizeof(int), cudaMemcpyDeviceToHost, s));
+      SCH_CUDA(ctx, cudaStreamSynchronize(s));
+      if (*ctx->h_flag) break;
+      chunk = std::min(chunk * 2, 32);
+    }
   }
   int ctl[3];
   double relres;
