@@ -436,6 +436,30 @@ def graph_bench(torch, sw, reps=10):
     return out
 
 
+def _device_for(local, torch):
+    """One GPU per rank.  SCH_DIST_BACKEND=gloo (control-flow tests of the
+    multi-rank bench on a 1-GPU box) maps ranks onto the visible devices."""
+    if os.environ.get("SCH_DIST_BACKEND") == "gloo":
+        return local % torch.cuda.device_count()
+    return local
+
+
+def _max_over_ranks(dist, torch, v):
+    """Max of a host float over all ranks (device tensor on NCCL, host on gloo)."""
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _init_dist(dist, torch, local):
+    backend = os.environ.get("SCH_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -451,9 +475,10 @@ def run_ours(args):
         if not args.no_stencil:
             cpu_stencil = cpu_stencil_baseline(min(args.cpu_seconds, 5.0))
 
+    local = _device_for(local, torch)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        _init_dist(dist, torch, local)
     import paper_1512_03812_b200 as sw
     from paper_1512_03812_b200 import _lib
     from paper_1512_03812_b200 import fermion as F
@@ -556,9 +581,7 @@ def run_ours(args):
     prof, F.CG_PROFILE = F.CG_PROFILE, None
     ms = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = _max_over_ranks(dist, torch, ms)
     ms_step = ms / args.steps
     value = chains * world / (ms_step * 1e-3)
 
@@ -656,9 +679,7 @@ def run_ours(args):
         barrier()
         ems = f0.elapsed_time(f1)
         if world > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+            ems = _max_over_ranks(dist, torch, ems)
         d2h = sum(b.numel() for b in q_back) * 8 + chains * (8 + 4)
         e2e = {"value": chains * world / (ems / steps_e2e * 1e-3), "unit": "chain-trajectories/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
