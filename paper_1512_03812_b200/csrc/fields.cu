@@ -12,10 +12,29 @@ namespace {
 constexpr double kPi = 3.141592653589793;      // np.pi
 constexpr double kTwoPi = 6.283185307179586;   // 2.0 * np.pi (lattice.py:21)
 
+// fmod(a, 2pi) without the library's bit-serial loop: n = trunc(a / 2pi)
+// from a rounded quotient, corrected by one if the rounding crossed an
+// integer; then a - n*2pi in one FMA.  The remainder of a division of two
+// doubles is exactly representable, so the single rounding of the FMA
+// returns it exactly: the result equals fmod's bit for bit.
+__device__ __forceinline__ double fmod_2pi(double a) {
+  if (!(fabs(a) < 1e15)) return fmod(a, kTwoPi);   // inf / nan / huge: the library path
+  double n = trunc(a * (1.0 / kTwoPi));
+  double r = __fma_rn(-n, kTwoPi, a);
+  if (r != 0.0 && (r < 0.0) != (a < 0.0)) {         // quotient rounded away from zero
+    n -= a < 0.0 ? -1.0 : 1.0;
+    r = __fma_rn(-n, kTwoPi, a);
+  } else if (fabs(r) >= kTwoPi) {                   // rounded toward zero past an integer
+    n += a < 0.0 ? -1.0 : 1.0;
+    r = __fma_rn(-n, kTwoPi, a);
+  }
+  return r;
+}
+
 // NumPy's floored remainder (npy_divmod) followed by -pi: lattice.py:28-30
 __device__ __forceinline__ double wrap_angle(double v) {
   double a = v + kPi;
-  double m = fmod(a, kTwoPi);
+  double m = fmod_2pi(a);
   if (m != 0.0) {
     if (m < 0.0) m += kTwoPi;
   } else {
@@ -114,12 +133,19 @@ __global__ void k_inner_leapfrog_resident(double* __restrict__ q, double* __rest
     sp[i] = pc[i];
   }
   __syncthreads();
+  // sin(theta) is recomputed only after a drift: the second half kick of a
+  // micro step and the first of the next act at the same links, so they share
+  // the force values (the kicks themselves stay separate, as in the reference)
+  bool fresh = false;
   auto kick = [&](double dt) {
-    for (int s = threadIdx.x; s < V; s += blockDim.x) {
-      int x = s / g.T, t = s - x * g.T;
-      ss[s] = sin(plaq(sq, g.L, g.T, x, t));
+    if (!fresh) {
+      for (int s = threadIdx.x; s < V; s += blockDim.x) {
+        int x = s / g.T, t = s - x * g.T;
+        ss[s] = sin(plaq(sq, g.L, g.T, x, t));
+      }
+      __syncthreads();
+      fresh = true;
     }
-    __syncthreads();
     for (int s = threadIdx.x; s < V; s += blockDim.x) {
       int x = s / g.T, t = s - x * g.T;
       int xm = x == 0 ? g.L - 1 : x - 1;
@@ -135,6 +161,7 @@ __global__ void k_inner_leapfrog_resident(double* __restrict__ q, double* __rest
   for (int k = 0; k < m; ++k) {
     if (half != 0.0) kick(half);
     for (int i = threadIdx.x; i < 2 * V; i += blockDim.x) sq[i] = wrap_angle(sq[i] + delta * sp[i]);
+    fresh = false;
     __syncthreads();
     if (half != 0.0) kick(half);
   }

@@ -364,3 +364,21 @@ def test_reject_returns_original_object(sw):
             return
         q = q_new
     pytest.fail("no rejection at a violently unstable step size")
+
+
+def test_wrap_angles_bit_exact_stress(sw):
+    """The device floored remainder (FMA with a corrected quotient instead of
+    the library fmod loop) is bit-identical to NumPy's on a million angles,
+    including exact multiples of 2pi, boundary neighbours and large values."""
+    from oracle import schwinger_oracle as O
+    rng = np.random.default_rng(2)
+    two_pi = 2.0 * np.pi
+    k = rng.integers(-40, 40, 200_000).astype(np.float64)
+    edge = np.concatenate([k * two_pi - np.pi, np.nextafter(k * two_pi - np.pi, np.inf),
+                           np.nextafter(k * two_pi - np.pi, -np.inf)])
+    vals = np.concatenate([rng.uniform(-4 * np.pi, 4 * np.pi, 300_000),
+                           rng.standard_normal(100_000) * 1e3, rng.standard_normal(50_000) * 1e9,
+                           edge, [0.0, -0.0, np.pi, -np.pi, 1e14, -1e14]])
+    got = sw.wrap_angles(vals).cpu().numpy()
+    want = O.wrap_angles(vals)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
