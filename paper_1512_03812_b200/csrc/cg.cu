@@ -58,60 +58,44 @@ int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
-template <int LC, int TC, int BX, int BT, int MINB, bool INC = false>
+template <int LC, int TC, int BX, int BT, int MINB>
 int launch_resblk(sch_ctx* ctx, const ResArgs& a, int B) {
   constexpr int NT = LC * TC / (BX * BT);
   const size_t smem = sizeof(double2) * 2 * (2 * BT + 2 * BX) * NT;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB, INC>,
+    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  k_cg_resblk<LC, TC, BX, BT, MINB, INC><<<B, NT, smem, ctx->stream>>>(a);
+  k_cg_resblk<LC, TC, BX, BT, MINB><<<B, NT, smem, ctx->stream>>>(a);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
 
-// Threads x sites-per-thread x min-CTAs-per-SM of the resident engine for V
-// sites; 16x16 and 32x32 get shape-specialised block-owned instantiations.
-// SCH_RESIDENT="NTxSPTxMINBxSPEC" overrides for tuning runs: SPEC 2 = block-
-// owned kernel with 1 x SPT blocks (resident_col.cuh), 3 = 2 x SPT/2 blocks,
-// 4 = 2 x SPT/2 with the incremental combine (default; 16^2 2.26 ns,
-// 32^2 10.76 ns per chain-iteration), 1 = the compile-time-shape strided
-// kernel, 0 = generic.
+// Resident-engine instantiation for V sites.  16x16 and 32x32 run the
+// block-owned kernel (2x2 sites per thread; resident_col.cuh: 16^2 2.26 ns,
+// 32^2 10.76 ns per chain-iteration); other shapes the strided kernel
+// (resident.cuh).  SCH_RESIDENT="NTxSPTxMINBxSPEC" forces a strided
+// instantiation for tuning runs (SPEC 1 = compile-time shape, 0 = generic).
 int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
-  static int fnt = -1, fspt = 0, fminb = 0, fspec = 4;
+  static int fnt = -1, fspt = 0, fminb = 0, fspec = 1;
   if (fnt < 0) {
     fnt = 0;
     if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%dx%dx%d", &fnt, &fspt, &fminb, &fspec);
   }
   const bool forced = fnt > 0 && (long long)fnt * fspt >= V;
+  if (!forced && a.L == 16 && a.T == 16) return launch_resblk<16, 16, 2, 2, 4>(ctx, a, B);
+  if (!forced && a.L == 32 && a.T == 32) return launch_resblk<32, 32, 2, 2, 1>(ctx, a, B);
   int nt, spt, minb;
   bool spec = true;
   if (forced) {
     nt = fnt; spt = fspt; minb = fminb; spec = fspec != 0;
   } else if (V <= 128) { nt = 128; spt = 1; minb = 1; }
-  else if (V == 256 && a.L == 16) { nt = 64; spt = 4; minb = 4; }
   else if (V <= 256) { nt = 128; spt = 2; minb = 4; }
   else if (V <= 512) { nt = 256; spt = 2; minb = 1; }
   else { nt = 256; spt = 4; minb = 1; }
-  const int blk = forced ? fspec : 4;   // 2: 1 x SPT, 3: 2 x SPT/2, 4: 2 x SPT/2 incremental
-  if (a.L == 16 && a.T == 16) {
-    if (blk == 2 && nt == 128 && spt == 2 && minb == 4) return launch_resblk<16, 16, 1, 2, 4>(ctx, a, B);
-    if (blk == 2 && nt == 64 && spt == 4 && minb == 4) return launch_resblk<16, 16, 1, 4, 4>(ctx, a, B);
-    if (blk == 3 && nt == 64 && spt == 4 && minb == 4) return launch_resblk<16, 16, 2, 2, 4>(ctx, a, B);
-    if (blk == 4 && nt == 64 && spt == 4 && minb == 4) return launch_resblk<16, 16, 2, 2, 4, true>(ctx, a, B);
-    if (blk == 4 && nt == 64 && spt == 4 && minb == 5) return launch_resblk<16, 16, 2, 2, 5, true>(ctx, a, B);
-    if (blk == 3 && nt == 128 && spt == 2 && minb == 4) return launch_resblk<16, 16, 2, 1, 4>(ctx, a, B);
-  }
-  if (a.L == 32 && a.T == 32) {
-    if (blk == 2 && nt == 256 && spt == 4 && minb == 1) return launch_resblk<32, 32, 1, 4, 1>(ctx, a, B);
-    if (blk == 3 && nt == 256 && spt == 4 && minb == 1) return launch_resblk<32, 32, 2, 2, 1>(ctx, a, B);
-    if (blk == 4 && nt == 256 && spt == 4 && minb == 1) return launch_resblk<32, 32, 2, 2, 1, true>(ctx, a, B);
-    if (blk == 2 && nt == 512 && spt == 2 && minb == 1) return launch_resblk<32, 32, 1, 2, 1>(ctx, a, B);
-  }
   const bool s16 = spec && a.L == 16 && a.T == 16 && (long long)nt * spt == 256;
   const bool s32 = spec && a.L == 32 && a.T == 32 && (long long)nt * spt == 1024;
 #define SCH_RES(N, S, M) \
@@ -120,8 +104,7 @@ int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
   if (s16 && nt == N && spt == S && minb == M) return launch_resident<N, S, M, 16, 16>(ctx, a, B);
 #define SCH_RES32(N, S, M) \
   if (s32 && nt == N && spt == S && minb == M) return launch_resident<N, S, M, 32, 32>(ctx, a, B);
-  SCH_RES16(128, 2, 4) SCH_RES16(128, 2, 5) SCH_RES16(256, 1, 4) SCH_RES16(256, 1, 5)
-  SCH_RES32(256, 4, 1) SCH_RES32(512, 2, 1)
+  SCH_RES16(128, 2, 4) SCH_RES32(256, 4, 1)
   SCH_RES(128, 1, 1) SCH_RES(128, 2, 1) SCH_RES(128, 2, 4)
   SCH_RES(256, 1, 4) SCH_RES(256, 2, 1) SCH_RES(256, 4, 1) SCH_RES(512, 2, 1)
 #undef SCH_RES
@@ -175,7 +158,7 @@ int cluster_dispatch(sch_ctx* ctx, const ResArgs& a, int B) {
   static int cs = -1;
   if (cs < 0) {
     cs = 4;   // measured (cfg4 shape): st.async/mbarrier variant 4 CTAs 67.2 ns/chain-iteration,
-              // 8 CTAs 67.8; cluster-barrier variant 4: 78.5, 8: 85, 16: 141 (spills)
+              // 8 CTAs 67.8; cluster-barrier variant (4 CTAs) 78.5
     if (const char* e = getenv("SCH_CLUSTER")) cs = atoi(e);
   }
   static int sync_mode = -1;
@@ -187,11 +170,7 @@ int cluster_dispatch(sch_ctx* ctx, const ResArgs& a, int B) {
     if (cs == 4) return launch_cluster_tx<64, 64, 4, 2, 2, 1>(ctx, a, B);
     if (cs == 8) return launch_cluster_tx<64, 64, 8, 2, 2, 2>(ctx, a, B);
   }
-  if (a.L == 64 && a.T == 64) {
-    if (cs == 8) return launch_cluster<64, 64, 8, 2, 2, 2>(ctx, a, B);
-    if (cs == 16) return launch_cluster<64, 64, 16, 2, 2, 4>(ctx, a, B);
-    if (cs == 4) return launch_cluster<64, 64, 4, 2, 2, 1>(ctx, a, B);
-  }
+  if (a.L == 64 && a.T == 64 && cs == 4) return launch_cluster<64, 64, 4, 2, 2, 1>(ctx, a, B);
   return -1;   // no cluster instantiation: use the streaming engine
 }
 

@@ -22,7 +22,7 @@
 
 #include <cooperative_groups.h>
 
-#include "resident_col.cuh"
+#include "block_stencil.cuh"
 #include "tma_tile.cuh"
 
 SCH_DEV void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
@@ -133,55 +133,21 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   const double t2 = target * target;
   const double t2lo = t2 * (1.0 - 4e-15), t2hi = t2 * (1.0 + 4e-15);
 
-  auto e0 = [&](auto dag, const Spinor& v) {
-    return decltype(dag)::value ? wplus0(v) : wminus0(v);
-  };
-  auto e1 = [&](auto dag, const Spinor& v, int k) {
-    return cmulc(u0[k], decltype(dag)::value ? wminus0(v) : wplus0(v));
-  };
-  auto e2 = [&](auto dag, const Spinor& v) {
-    return decltype(dag)::value ? wplus1(v) : wminus1(v);
-  };
-  auto e3 = [&](auto dag, const Spinor& v, int k) {
-    return cmulc(u1[k], decltype(dag)::value ? wminus1(v) : wplus1(v));
-  };
+  using Blk = SiteBlock<BX, BT>;
   auto produce = [&](auto dag, double2* E, const Spinor* v) {
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      if (i == 0) E[O0 + j * NT + tid] = e0(dag, v[k]);
-      if (i == BX - 1) E[O1 + j * NT + tid] = e1(dag, v[k], k);
-      if (j == 0) E[O2 + i * NT + tid] = e2(dag, v[k]);
-      if (j == BT - 1) E[O3 + i * NT + tid] = e3(dag, v[k], k);
-    }
+    Blk::template produce<decltype(dag)::value>(u0, u1, v, [&](int plane, int idx, double2 val) {
+      constexpr int off[4] = {O0, O1, O2, O3};
+      E[off[plane] + idx * NT + tid] = val;
+    });
   };
   // interior: out = diag*v + the hops between this thread's own sites
   // (register-only; runs between arrive and wait of the exchange barrier)
   auto interior = [&](auto dag, const Spinor* v, Spinor* out) {
-    constexpr bool DAG = decltype(dag)::value;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      bool first = true;
-      if (i < BX - 1) {
-        hop_acc<DAG, 0>(out[k], cmul(u0[k], e0(dag, v[k + BT])), first, v[k], a.diag);
-        first = false;
-      }
-      if (i > 0) {
-        hop_acc<DAG, 1>(out[k], e1(dag, v[k - BT], k - BT), first, v[k], a.diag);
-        first = false;
-      }
-      if (j < BT - 1) {
-        hop_acc<DAG, 2>(out[k], cmul(u1[k], e2(dag, v[k + 1])), first, v[k], a.diag);
-        first = false;
-      }
-      if (j > 0) hop_acc<DAG, 3>(out[k], e3(dag, v[k - 1], k - 1), first, v[k], a.diag);
-    }
+    Blk::template interior<decltype(dag)::value>(u0, u1, v, out, a.diag);
   };
   // faces: add the hops exported by the neighbouring blocks (x-faces possibly
   // from the neighbouring CTA's shared memory); all loads issued first
   auto faces = [&](auto dag, const double2* E, uint32_t stage_off, Spinor* out) {
-    constexpr bool DAG = decltype(dag)::value;
     double2 fx[SPT], ft[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
@@ -191,16 +157,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
       if (j == BT - 1) ft[k] = E[O2 + i * NT + ttp];
       if (j == 0) ft[k] = E[O3 + i * NT + ttm];
     }
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      if (i == BX - 1) hop_acc<DAG, 0>(out[k], cmul(u0[k], fx[k]), false, out[k], 0.0);
-      if (i == 0) hop_acc<DAG, 1>(out[k], fx[k], false, out[k], 0.0);
-      if (j == BT - 1) hop_acc<DAG, 2>(out[k], cmul(u1[k], ft[k]), false, out[k], 0.0);
-      if (j == 0) hop_acc<DAG, 3>(out[k], ft[k], false, out[k], 0.0);
-    }
+    Blk::template faces<decltype(dag)::value>(u0, u1, fx, ft, out);
   };
-  static_assert(BX >= 2 && BT >= 2, "interior() needs an internal hop in both directions");
   using F = std::integral_constant<bool, false>;
   using T = std::integral_constant<bool, true>;
 
@@ -477,60 +435,25 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   const double t2 = target * target;
   const double t2lo = t2 * (1.0 - 4e-15), t2hi = t2 * (1.0 + 4e-15);
 
-  auto e0 = [&](auto dag, const Spinor& v) { return decltype(dag)::value ? wplus0(v) : wminus0(v); };
-  auto e1 = [&](auto dag, const Spinor& v, int k) {
-    return cmulc(u0[k], decltype(dag)::value ? wminus0(v) : wplus0(v));
-  };
-  auto e2 = [&](auto dag, const Spinor& v) { return decltype(dag)::value ? wplus1(v) : wminus1(v); };
-  auto e3 = [&](auto dag, const Spinor& v, int k) {
-    return cmulc(u1[k], decltype(dag)::value ? wminus1(v) : wplus1(v));
-  };
+  using Blk = SiteBlock<BX, BT>;
   // produce stage s: local planes, and the CTA's edge rows pushed to the
   // neighbouring CTAs' receive buffers
   auto produce = [&](auto dag, int s, const Spinor* v) {
     double2* E = E0 + s * PL;
     const int q = ufx[s] & 1;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      if (i == 0) {
-        const double2 val = e0(dag, v[k]);
-        if (bx == 0)   // read by rank-1's last block row as its forward-x hop
-          st_async_v2f64(pushP + 16u * ((s * 2 + q) * FACE + j * NBT), val, barP + 8u * (s * 2 + q));
-        else
-          E[O0 + j * NT + tid] = val;
+    Blk::template produce<decltype(dag)::value>(u0, u1, v, [&](int plane, int idx, double2 val) {
+      if (plane == 0 && bx == 0)   // read by rank-1's last block row as its forward-x hop
+        st_async_v2f64(pushP + 16u * ((s * 2 + q) * FACE + idx * NBT), val, barP + 8u * (s * 2 + q));
+      else if (plane == 1 && bx == NBX - 1)   // read by rank+1's first block row (backward-x)
+        st_async_v2f64(pushM + 16u * ((s * 2 + q) * FACE + idx * NBT), val, barM + 8u * (s * 2 + q));
+      else {
+        constexpr int off[4] = {O0, O1, O2, O3};
+        E[off[plane] + idx * NT + tid] = val;
       }
-      if (i == BX - 1) {
-        const double2 val = e1(dag, v[k], k);
-        if (bx == NBX - 1)   // read by rank+1's first block row as its backward-x hop
-          st_async_v2f64(pushM + 16u * ((s * 2 + q) * FACE + j * NBT), val, barM + 8u * (s * 2 + q));
-        else
-          E[O1 + j * NT + tid] = val;
-      }
-      if (j == 0) E[O2 + i * NT + tid] = e2(dag, v[k]);
-      if (j == BT - 1) E[O3 + i * NT + tid] = e3(dag, v[k], k);
-    }
+    });
   };
   auto interior = [&](auto dag, const Spinor* v, Spinor* out) {
-    constexpr bool DAG = decltype(dag)::value;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      bool first = true;
-      if (i < BX - 1) {
-        hop_acc<DAG, 0>(out[k], cmul(u0[k], e0(dag, v[k + BT])), first, v[k], a.diag);
-        first = false;
-      }
-      if (i > 0) {
-        hop_acc<DAG, 1>(out[k], e1(dag, v[k - BT], k - BT), first, v[k], a.diag);
-        first = false;
-      }
-      if (j < BT - 1) {
-        hop_acc<DAG, 2>(out[k], cmul(u1[k], e2(dag, v[k + 1])), first, v[k], a.diag);
-        first = false;
-      }
-      if (j > 0) hop_acc<DAG, 3>(out[k], e3(dag, v[k - 1], k - 1), first, v[k], a.diag);
-    }
+    Blk::template interior<decltype(dag)::value>(u0, u1, v, out, a.diag);
   };
   auto faces = [&](auto dag, int s, Spinor* out) {
     constexpr bool DAG = decltype(dag)::value;
@@ -549,14 +472,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
       if (j == BT - 1) ft[k] = E[O2 + i * NT + ttp];
       if (j == 0) ft[k] = E[O3 + i * NT + ttm];
     }
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      if (i == BX - 1) hop_acc<DAG, 0>(out[k], cmul(u0[k], fx[k]), false, out[k], 0.0);
-      if (i == 0) hop_acc<DAG, 1>(out[k], fx[k], false, out[k], 0.0);
-      if (j == BT - 1) hop_acc<DAG, 2>(out[k], cmul(u1[k], ft[k]), false, out[k], 0.0);
-      if (j == 0) hop_acc<DAG, 3>(out[k], ft[k], false, out[k], 0.0);
-    }
+    Blk::template faces<DAG>(u0, u1, fx, ft, out);
     ++ufx[s];
   };
   using F = std::integral_constant<bool, false>;

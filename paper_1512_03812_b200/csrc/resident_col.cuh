@@ -1,34 +1,34 @@
-// Resident per-chain CG, block-owned variant (the 16^2 / 32^2 hot shapes).
+// Resident per-chain CG, block-owned (the 16^2 / 32^2 hot shapes).
 //
 // Same algorithm, stopping rule and data placement as k_cg_resident
 // (resident.cuh), but each thread owns a BX x BT block of sites (BX rows in
-// x, BT consecutive sites in t) instead of sites strided by the block size.
-// Hops between a thread's own sites never leave its registers; per D
-// application a block exports to shared memory only its faces:
+// x, BT consecutive sites in t; block_stencil.cuh) instead of sites strided
+// by the block size.  Per D application a block exports only its faces:
 //   plane 0 (read by x-1): the BT sites of its first row
 //   plane 1 (read by x+1): the BT sites of its last row
 //   plane 2 (read by t-1): the BX sites of its first column
 //   plane 3 (read by t+1): the BX sites of its last column
 // i.e. 2(BX+BT) projected components per BX*BT sites instead of 4 per site
-// (1x2: -25 %, 1x4: -37.5 %, 2x2: -50 % shared-memory traffic).  Internal
-// hops are formed after the barrier straight from the neighbour site's
-// registers, so nothing extra stays live across it.  Planes are indexed by
+// (2x2: -50 % shared-memory traffic).  The register-only internal hops are
+// summed while the exchange barrier is pending.  Planes are indexed by
 // thread id: every warp-wide store and neighbour load is one contiguous (or
 // lane-permuted within aligned 128-B groups) run — conflict-free.
 //
 // The per-iteration stopping test sqrt(rs') <= target (fermion.py:202) is
 // decided without the square root unless rs' falls inside a +-4e-15 band
 // around target^2, where the exact comparison is evaluated: the decision is
-// the one the reference takes, at two compares per iteration.
+// the one the reference takes, at two compares per iteration.  beta = rs'/rs
+// is finished from a reciprocal formed off the critical path (Markstein:
+// q0 = rs'*y, rem = rs' - rs*q0 exact, q = q0 + rem*y is correctly rounded
+// for y = RN(1/rs)), three dependent operations instead of a division.
 #pragma once
 
-#include <type_traits>
+#include "block_stencil.cuh"
 
-#include "resident.cuh"
-
-template <int LC, int TC, int BX, int BT, int MINB, bool INC = false>
+template <int LC, int TC, int BX, int BT, int MINB>
 __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs a) {
-  constexpr int SPT = BX * BT;
+  using Blk = SiteBlock<BX, BT>;
+  constexpr int SPT = Blk::SPT;
   constexpr int NT = LC * TC / SPT;
   constexpr int NBT = TC / BT, NBX = LC / BX;
   constexpr int V = LC * TC;
@@ -79,124 +79,42 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
   const double t2 = target * target;
   const double t2lo = t2 * (1.0 - 4e-15), t2hi = t2 * (1.0 + 4e-15);
 
-  // The four exports of site k (D: DAG=false, D^dag: DAG=true), res_produce
-  // order: e0 = w_f0(v), e1 = conj(u0) w_b0(v), e2 = w_f1(v), e3 = conj(u1) w_b1(v)
-  auto e0 = [&](auto dag, const Spinor& v) {
-    return decltype(dag)::value ? wplus0(v) : wminus0(v);
-  };
-  auto e1 = [&](auto dag, const Spinor& v, int k) {
-    return cmulc(u0[k], decltype(dag)::value ? wminus0(v) : wplus0(v));
-  };
-  auto e2 = [&](auto dag, const Spinor& v) {
-    return decltype(dag)::value ? wplus1(v) : wminus1(v);
-  };
-  auto e3 = [&](auto dag, const Spinor& v, int k) {
-    return cmulc(u1[k], decltype(dag)::value ? wminus1(v) : wplus1(v));
-  };
-  // produce: the block's face exports of v
-  auto produce = [&](auto dag, double2* E, const Spinor* v) {
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      if (i == 0) E[O0 + j * NT + tid] = e0(dag, v[k]);
-      if (i == BX - 1) E[O1 + j * NT + tid] = e1(dag, v[k], k);
-      if (j == 0) E[O2 + i * NT + tid] = e2(dag, v[k]);
-      if (j == BT - 1) E[O3 + i * NT + tid] = e3(dag, v[k], k);
-    }
-  };
-  // gather: the four hops of every site (faces from shared memory, internal
-  // ones from the neighbour site's registers)
-  auto gather = [&](auto dag, const double2* E, const Spinor* v, Hops* h) {
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      if (i == BX - 1) h[k].f0 = E[O0 + j * NT + txp];
-      if (i == 0) h[k].b0 = E[O1 + j * NT + txm];
-      if (j == BT - 1) h[k].f1 = E[O2 + i * NT + ttp];
-      if (j == 0) h[k].b1 = E[O3 + i * NT + ttm];
-    }
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      if (i < BX - 1) h[k].f0 = e0(dag, v[k + BT]);
-      if (i > 0) h[k].b0 = e1(dag, v[k - BT], k - BT);
-      if (j < BT - 1) h[k].f1 = e2(dag, v[k + 1]);
-      if (j > 0) h[k].b1 = e3(dag, v[k - 1], k - 1);
-    }
-  };
-  using F = std::integral_constant<bool, false>;
-  using T = std::integral_constant<bool, true>;
-  // INC: incremental combine (resident.cuh hop_acc) — the register-only
-  // internal hops are summed before the exchange barrier, the face hops after
-  auto interior = [&](auto dag, const Spinor* v, Spinor* out) {
+  // One exchange stage, split around its barrier: exports + interior hops
+  // before, face loads + face hops after.
+  auto stage_pre = [&](auto dag, double2* E, const Spinor* v, Spinor* out) {
     constexpr bool DAG = decltype(dag)::value;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      bool first = true;
-      if (i < BX - 1) {
-        hop_acc<DAG, 0>(out[k], cmul(u0[k], e0(dag, v[k + BT])), first, v[k], a.diag);
-        first = false;
-      }
-      if (i > 0) {
-        hop_acc<DAG, 1>(out[k], e1(dag, v[k - BT], k - BT), first, v[k], a.diag);
-        first = false;
-      }
-      if (j < BT - 1) {
-        hop_acc<DAG, 2>(out[k], cmul(u1[k], e2(dag, v[k + 1])), first, v[k], a.diag);
-        first = false;
-      }
-      if (j > 0) hop_acc<DAG, 3>(out[k], e3(dag, v[k - 1], k - 1), first, v[k], a.diag);
-    }
+    Blk::template produce<DAG>(u0, u1, v, [&](int plane, int idx, double2 val) {
+      constexpr int off[4] = {O0, O1, O2, O3};
+      E[off[plane] + idx * NT + tid] = val;
+    });
+    Blk::template interior<DAG>(u0, u1, v, out, a.diag);
   };
-  auto faces = [&](auto dag, const double2* E, Spinor* out) {
+  auto stage_post = [&](auto dag, const double2* E, Spinor* out) {
     constexpr bool DAG = decltype(dag)::value;
     double2 fx[SPT], ft[SPT];
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) {
+    for (int k = 0; k < SPT; ++k) {   // all face loads in flight before any math
       const int i = k / BT, j = k % BT;
       if (i == BX - 1) fx[k] = E[O0 + j * NT + txp];
       if (i == 0) fx[k] = E[O1 + j * NT + txm];
       if (j == BT - 1) ft[k] = E[O2 + i * NT + ttp];
       if (j == 0) ft[k] = E[O3 + i * NT + ttm];
     }
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      if (i == BX - 1) hop_acc<DAG, 0>(out[k], cmul(u0[k], fx[k]), false, out[k], 0.0);
-      if (i == 0) hop_acc<DAG, 1>(out[k], fx[k], false, out[k], 0.0);
-      if (j == BT - 1) hop_acc<DAG, 2>(out[k], cmul(u1[k], ft[k]), false, out[k], 0.0);
-      if (j == 0) hop_acc<DAG, 3>(out[k], ft[k], false, out[k], 0.0);
-    }
+    Blk::template faces<DAG>(u0, u1, fx, ft, out);
   };
-  static_assert(!INC || (BX >= 2 && BT >= 2), "incremental combine needs internal hops both ways");
+  using F = std::integral_constant<bool, false>;
+  using T = std::integral_constant<bool, true>;
 
   // out = D^dag D v (two exchange rounds).  Precondition: every thread has
   // finished reading E0/E1 of the previous application.
   auto normal_op = [&](const Spinor* v, Spinor* out) {
-    if constexpr (INC) {
-      Spinor t[SPT];
-      produce(F{}, E0, v);
-      interior(F{}, v, t);
-      __syncthreads();
-      faces(F{}, E0, t);
-      produce(T{}, E1, t);
-      interior(T{}, t, out);
-      __syncthreads();
-      faces(T{}, E1, out);
-    } else {
-      Hops h[SPT];
-      produce(F{}, E0, v);
-      __syncthreads();
-      gather(F{}, E0, v, h);
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) out[k] = res_combine<false>(h[k], v[k], u0[k], u1[k], a.diag);
-      produce(T{}, E1, out);
-      __syncthreads();
-      gather(T{}, E1, out, h);
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) out[k] = res_combine<true>(h[k], out[k], u0[k], u1[k], a.diag);
-    }
+    Spinor t[SPT];
+    stage_pre(F{}, E0, v, t);
+    __syncthreads();
+    stage_post(F{}, E0, t);
+    stage_pre(T{}, E1, t, out);
+    __syncthreads();
+    stage_post(T{}, E1, out);
   };
 
   Spinor w[SPT];
@@ -221,39 +139,19 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
   for (int it = 1; it <= a.maxiter; ++it) {
     // w = D^dag D p; <p, D^dag D p> formed as ||D p||^2 during the D stage
     // and published by the barrier between the stages (resident.cuh)
-    if constexpr (INC) {
+    {
       Spinor t[SPT];
-      produce(F{}, E0, p);
-      interior(F{}, p, t);
+      stage_pre(F{}, E0, p, t);
       __syncthreads();
-      faces(F{}, E0, t);
+      stage_post(F{}, E0, t);
       double dd = 0.0;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) dd += spinor_norm2(t[k]);
-      produce(T{}, E1, t);
-      interior(T{}, t, w);
+      stage_pre(T{}, E1, t, w);
       dd = warp_sum(dd);
       if ((tid & 31) == 0) red[0][tid >> 5] = dd;
       __syncthreads();
-      faces(T{}, E1, w);
-    } else {
-      Hops h[SPT];
-      produce(F{}, E0, p);
-      __syncthreads();
-      gather(F{}, E0, p, h);
-      double dd = 0.0;
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) {
-        w[k] = res_combine<false>(h[k], p[k], u0[k], u1[k], a.diag);
-        dd += spinor_norm2(w[k]);
-      }
-      produce(T{}, E1, w);
-      dd = warp_sum(dd);
-      if ((tid & 31) == 0) red[0][tid >> 5] = dd;
-      __syncthreads();
-      gather(T{}, E1, w, h);
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) w[k] = res_combine<true>(h[k], w[k], u0[k], u1[k], a.diag);
+      stage_post(T{}, E1, w);
     }
     double den = red[0][0];
 #pragma unroll
@@ -305,10 +203,7 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
       for (int k = 0; k < SPT; ++k) r[k] = w[k];
       rs_new = tn2;
     }
-    // rs'/rs finished from the reciprocal formed off the critical path:
-    // q0 = rs'*y, rem = rs' - rs*q0 (exact), q = q0 + rem*y -- the correctly
-    // rounded quotient for y = RN(1/rs) (Markstein), in 3 dependent ops
-    double beta = 0.0;
+    double beta = 0.0;   // Markstein-finished rs'/rs (header comment)
     if (rs > 0.0) {
       const double q0 = rs_new * inv_rs;
       beta = __fma_rn(__fma_rn(-rs, q0, rs_new), inv_rs, q0);
