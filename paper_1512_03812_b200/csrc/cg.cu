@@ -253,6 +253,7 @@ __global__ void k_copy_r_to_p(ElemArgs e) {
 // the chain's <p,Ap> tile partials, in the same fixed order as k_ctrl_alpha.
 template <bool FUSE_ALPHA>
 __global__ void k_cg_update(ElemArgs e, StreamState st) {
+  pdl_enter();
   __shared__ double slot[32];
   const int repl = (*st.it % kReplace) == 0;
   const int c = blockIdx.x / e.tpc, tile = blockIdx.x - c * e.tpc;
@@ -367,6 +368,7 @@ __global__ void k_ctrl_init_global(StreamState st) {
 // after the stencil pass: alpha = <p,Ap> > 0 ? rs/<p,Ap> : 0
 template <bool PT>
 __global__ void k_ctrl_alpha(StreamState st) {
+  pdl_enter();
   __shared__ double slot[32];
   const int c = ctrl_chain<PT>();
   if (c >= st.B || !st.active[c]) return;
@@ -377,6 +379,7 @@ __global__ void k_ctrl_alpha(StreamState st) {
 // after the update: rs' and the convergence check
 template <bool PT>
 __global__ void k_ctrl_check(StreamState st) {
+  pdl_enter();
   __shared__ double slot[32];
   const int repl = (*st.it % kReplace) == 0;
   const int c = ctrl_chain<PT>();
@@ -399,6 +402,7 @@ __global__ void k_ctrl_check(StreamState st) {
 
 // global mode: the true-residual branch runs only when every chain passes
 __global__ void k_ctrl_check_global(StreamState st) {
+  pdl_enter();
   const int repl = (*st.it % kReplace) == 0;
   __shared__ int fails;
   if (threadIdx.x == 0) fails = 0;
@@ -415,6 +419,7 @@ __global__ void k_ctrl_check_global(StreamState st) {
 // after the (optional) true-residual pass
 template <bool PT>
 __global__ void k_ctrl_final(StreamState st) {
+  pdl_enter();
   __shared__ double slot[32];
   const int it = *st.it;
   const int c = ctrl_chain<PT>();
@@ -451,6 +456,7 @@ __global__ void k_ctrl_final(StreamState st) {
 }
 
 __global__ void k_ctrl_final_global(StreamState st) {
+  pdl_enter();
   const int it = *st.it;
   __shared__ int fails, any_x;
   __shared__ double worst;
@@ -502,12 +508,14 @@ __global__ void k_ctrl_final_global(StreamState st) {
 }
 
 __global__ void k_iter_inc(StreamState st) {
+  pdl_enter();
   if (threadIdx.x == 0) ++*st.it;
 }
 
 // Body tail of the device-side CG loop: keep iterating while a chain is
 // active (the WHILE node of the conditional graph re-evaluates this).
 __global__ void k_set_continue(StreamState st, cudaGraphConditionalHandle h) {
+  pdl_enter();
   if (threadIdx.x == 0)
     cudaGraphSetConditional(h, (*st.n_active > 0 && *st.it <= st.maxiter + 1) ? 1u : 0u);
 }
@@ -636,35 +644,39 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
   // One CG iteration; every decision (replacement, convergence, maxiter)
   // is made on the device from st.it, so the sequence can be captured once
   // and replayed.  Returns the number of kernels enqueued.
+  // Every launch but the first of a solve uses programmatic stream
+  // serialization (runtime.hpp launch_k): its CTAs are scheduled while the
+  // previous kernel drains and wait in pdl_enter().
+  const bool pdl = use_pdl();
   auto enqueue_iteration = [&](cudaStream_t q) -> int {
     int n = 0;
     if (tma_p) launch_normal_tma<MODE_P>(tp, q, ctx->num_sms);
-    else launch_normal_tile<MODE_P>(sh, tp, q);
+    else launch_normal_tile<MODE_P>(sh, tp, q, 0, pdl);
     ++n;
     if (pt) {
-      k_cg_update<true><<<ngrid, 256, 0, q>>>(e, st);
-      k_ctrl_check<true><<<cgrid, 128, 0, q>>>(st);
+      launch_k(pdl, k_cg_update<true>, dim3(ngrid), dim3(256), 0, q, e, st);
+      launch_k(pdl, k_ctrl_check<true>, dim3(cgrid), dim3(128), 0, q, st);
       n += 2;
     } else {
-      k_ctrl_alpha<false><<<cgrid, 128, 0, q>>>(st);
-      k_cg_update<false><<<ngrid, 256, 0, q>>>(e, st);
-      k_ctrl_check<false><<<cgrid, 128, 0, q>>>(st);
+      launch_k(pdl, k_ctrl_alpha<false>, dim3(cgrid), dim3(128), 0, q, st);
+      launch_k(pdl, k_cg_update<false>, dim3(ngrid), dim3(256), 0, q, e, st);
+      launch_k(pdl, k_ctrl_check<false>, dim3(cgrid), dim3(128), 0, q, st);
       n += 3;
     }
     if (global_mode) {
-      k_ctrl_check_global<<<1, 1024, 0, q>>>(st);
+      launch_k(pdl, k_ctrl_check_global, dim3(1), dim3(1024), 0, q, st);
       ++n;
     }
-    launch_normal_tile<MODE_X>(sh, txx, q, sparse);
+    launch_normal_tile<MODE_X>(sh, txx, q, sparse, pdl);
     ++n;
-    if (pt) k_ctrl_final<true><<<cgrid, 128, 0, q>>>(st);
-    else k_ctrl_final<false><<<cgrid, 128, 0, q>>>(st);
+    if (pt) launch_k(pdl, k_ctrl_final<true>, dim3(cgrid), dim3(128), 0, q, st);
+    else launch_k(pdl, k_ctrl_final<false>, dim3(cgrid), dim3(128), 0, q, st);
     ++n;
     if (global_mode) {
-      k_ctrl_final_global<<<1, 1024, 0, q>>>(st);
+      launch_k(pdl, k_ctrl_final_global, dim3(1), dim3(1024), 0, q, st);
       ++n;
     }
-    k_iter_inc<<<1, 32, 0, q>>>(st);
+    launch_k(pdl, k_iter_inc, dim3(1), dim3(32), 0, q, st);
     return n + 1;
   };
   auto poll_done = [&]() -> int {
@@ -677,7 +689,14 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
     // The whole loop on the device: a conditional WHILE node whose body is
     // kBody captured iterations plus k_set_continue.  One graph launch per
     // solve, no host polling: the call returns without synchronising.
-    const int kBody = tpc * B >= 4096 ? 1 : 4;   // big batches: exact trip count
+    static int kb = -1;
+    if (kb < 0) {
+      const char* ev = getenv("SCH_CG_BODY");
+      kb = ev ? atoi(ev) : 0;
+    }
+    // 4 iterations per pass of the WHILE body: the conditional node costs
+    // ~3.5 us per evaluation, a converged iteration is a few no-op launches
+    const int kBody = kb > 0 ? kb : 4;
     if (!ctx->cap_stream)
       SCH_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
     cudaGraph_t graph;
@@ -696,7 +715,7 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
                                                 cudaStreamCaptureModeRelaxed));
     int per = 0;
     for (int j = 0; j < kBody; ++j) per += enqueue_iteration(ctx->cap_stream);
-    k_set_continue<<<1, 32, 0, ctx->cap_stream>>>(st, handle);
+    launch_k(pdl, k_set_continue, dim3(1), dim3(32), 0, ctx->cap_stream, st, handle);
     cudaError_t ce = cudaGetLastError();
     SCH_CUDA(ctx, cudaStreamEndCapture(ctx->cap_stream, &body));
     if (ce != cudaSuccess) {

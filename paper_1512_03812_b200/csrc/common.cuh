@@ -162,6 +162,17 @@ SCH_DEV double block_sum_rt(double v, double* slot) {
 
 SCH_DEV int wrapi(int i, int n) { return i < 0 ? i + n : (i >= n ? i - n : i); }
 
+// Programmatic dependent launch (sm_90+).  A kernel launched with the
+// programmatic-stream-serialization attribute may be scheduled while its
+// predecessor drains: kernels that take part call pdl_enter() first — it
+// lets their own successor launch early and then waits until the
+// predecessor has completed and its writes are visible.  Under a normal
+// launch both instructions are no-ops.
+SCH_DEV void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // theta(n) = q0(n) + q1(n+x) - q0(n+t) - q1(n)   (gauge.py:21-24), NumPy order.
 // qc points at one chain's [2][L][T] angles.
 SCH_DEV double plaq(const double* __restrict__ qc, int L, int T, int x, int t) {

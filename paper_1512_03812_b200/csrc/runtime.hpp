@@ -96,6 +96,38 @@ inline int sch_workspace(sch_ctx* c, size_t bytes, void** out) {
 
 inline unsigned blocks_for(long n, int nt) { return (unsigned)((n + nt - 1) / nt); }
 
+// Streaming-CG kernels are launched with programmatic stream serialization
+// (common.cuh pdl_enter) so each one's launch overlaps its predecessor's
+// tail; SCH_NO_PDL=1 launches them plainly.
+inline bool use_pdl() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SCH_NO_PDL");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_k(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args... args) {
+  if (!pdl) {
+    kern<<<grid, block, smem, st>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);   // errors surface through cudaGetLastError
+}
+
 // The TMA-pipelined stencil is the default where its tile shapes apply;
 // SCH_NO_TMA=1 selects the plain per-tile kernels (A/B measurements).
 inline bool use_tma() {

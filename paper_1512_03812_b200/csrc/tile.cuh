@@ -27,6 +27,7 @@
 
 #include "common.cuh"
 #include "resident.cuh"
+#include "runtime.hpp"
 
 enum { MODE_PLAIN = 0, MODE_P = 1, MODE_X = 2 };
 
@@ -165,6 +166,7 @@ __global__ void __launch_bounds__(NT, MINB) k_normal_tile(TileArgs a) {
   extern __shared__ double2 E[];            // [4][NR] exported projections (dynamic)
   __shared__ int gx[RX], gxm[RX], gt[RT], gtm[RT];
   __shared__ double slot[NT / 32];
+  pdl_enter();
   const int c = blockIdx.x / a.tiles_per_chain;
   const int tile = blockIdx.x - c * a.tiles_per_chain;
   if (MODE != MODE_PLAIN && a.flag && a.flag[c] == 0) return;
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(NT, MINB) k_normal_tile_sparse(TileArgs a) {
   __shared__ int gx[RX], gxm[RX], gt[RT], gtm[RT];
   __shared__ double slot[NT / 32];
   __shared__ unsigned mask;
+  pdl_enter();
   const int ntiles = a.B * a.tiles_per_chain;
   // chunks of 32 tiles: warp 0 reads the 32 flags in parallel, the CTA then
   // walks the set bits (an idle pass costs one flag read per chunk)
@@ -245,7 +248,7 @@ inline TileShape pick_tile(int L, int T, bool tma = false) {
 }
 
 template <int TX, int TT, int HX, int HT, int MODE, int NT, int MINB>
-inline void launch_tile_inst(const TileArgs& a, cudaStream_t st, int sparse_grid) {
+inline void launch_tile_inst(const TileArgs& a, cudaStream_t st, int sparse_grid, bool pdl) {
   constexpr int NR = (TX + 2 * HX) * (TT + 2 * HT);
   constexpr size_t smem = sizeof(double2) * 4 * NR;
   static bool attr = false;
@@ -257,28 +260,30 @@ inline void launch_tile_inst(const TileArgs& a, cudaStream_t st, int sparse_grid
     attr = true;
   }
   if (sparse_grid > 0)
-    k_normal_tile_sparse<TX, TT, HX, HT, MODE, NT, MINB><<<sparse_grid, NT, smem, st>>>(a);
+    launch_k(pdl, k_normal_tile_sparse<TX, TT, HX, HT, MODE, NT, MINB>, dim3(sparse_grid), dim3(NT),
+             smem, st, a);
   else
-    k_normal_tile<TX, TT, HX, HT, MODE, NT, MINB><<<(unsigned)a.B * a.tiles_per_chain, NT, smem, st>>>(a);
+    launch_k(pdl, k_normal_tile<TX, TT, HX, HT, MODE, NT, MINB>, dim3((unsigned)a.B * a.tiles_per_chain),
+             dim3(NT), smem, st, a);
 }
 
 // Launch the instantiation matching `sh`.  sparse_grid > 0 selects the
 // persistent flag-skipping variant with that many CTAs.
 template <int MODE>
 inline void launch_normal_tile(const TileShape& sh, const TileArgs& a, cudaStream_t st,
-                               int sparse_grid = 0) {
+                               int sparse_grid = 0, bool pdl = false) {
   switch (sh.kind) {
-    case 0: launch_tile_inst<16, 16, 0, 0, MODE, 256, 3>(a, st, sparse_grid); break;
-    case 1: launch_tile_inst<16, 32, 2, 0, MODE, 512, 2>(a, st, sparse_grid); break;
-    case 2: launch_tile_inst<8, 64, 2, 0, MODE, 512, 2>(a, st, sparse_grid); break;
-    case 3: launch_tile_inst<16, 64, 2, 2, MODE, 512, 2>(a, st, sparse_grid); break;
-    case 5: launch_tile_inst<8, 32, 2, 0, MODE, 384, 2>(a, st, sparse_grid); break;
-    case 6: launch_tile_inst<16, 16, 2, 0, MODE, 320, 2>(a, st, sparse_grid); break;
-    case 7: launch_tile_inst<4, 64, 2, 0, MODE, 512, 2>(a, st, sparse_grid); break;
-    case 8: launch_tile_inst<4, 32, 2, 0, MODE, 256, 3>(a, st, sparse_grid); break;
-    case 9: launch_tile_inst<8, 32, 2, 0, MODE, 128, 4>(a, st, sparse_grid); break;
-    case 10: launch_tile_inst<16, 32, 2, 0, MODE, 256, 3>(a, st, sparse_grid); break;
-    case 11: launch_tile_inst<16, 32, 2, 0, MODE, 128, 4>(a, st, sparse_grid); break;
-    default: launch_tile_inst<8, 16, 2, 2, MODE, 128, 4>(a, st, sparse_grid); break;
+    case 0: launch_tile_inst<16, 16, 0, 0, MODE, 256, 3>(a, st, sparse_grid, pdl); break;
+    case 1: launch_tile_inst<16, 32, 2, 0, MODE, 512, 2>(a, st, sparse_grid, pdl); break;
+    case 2: launch_tile_inst<8, 64, 2, 0, MODE, 512, 2>(a, st, sparse_grid, pdl); break;
+    case 3: launch_tile_inst<16, 64, 2, 2, MODE, 512, 2>(a, st, sparse_grid, pdl); break;
+    case 5: launch_tile_inst<8, 32, 2, 0, MODE, 384, 2>(a, st, sparse_grid, pdl); break;
+    case 6: launch_tile_inst<16, 16, 2, 0, MODE, 320, 2>(a, st, sparse_grid, pdl); break;
+    case 7: launch_tile_inst<4, 64, 2, 0, MODE, 512, 2>(a, st, sparse_grid, pdl); break;
+    case 8: launch_tile_inst<4, 32, 2, 0, MODE, 256, 3>(a, st, sparse_grid, pdl); break;
+    case 9: launch_tile_inst<8, 32, 2, 0, MODE, 128, 4>(a, st, sparse_grid, pdl); break;
+    case 10: launch_tile_inst<16, 32, 2, 0, MODE, 256, 3>(a, st, sparse_grid, pdl); break;
+    case 11: launch_tile_inst<16, 32, 2, 0, MODE, 128, 4>(a, st, sparse_grid, pdl); break;
+    default: launch_tile_inst<8, 16, 2, 2, MODE, 128, 4>(a, st, sparse_grid, pdl); break;
   }
 }
