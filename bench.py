@@ -56,8 +56,8 @@ FALLBACK_HBM = 6650.0
 #         the true-residual checks; part of it misses L2)
 DRAM_CFG4 = (268.8832e6 + 103.359744e6) / (1024 * 4096)
 CG_KERNELS = {
-    "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread,incremental> (per-chain CG, one "
-                        "64-thread CTA per chain, 4 CTAs/SM)",
+    "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread,t-faces by warp shuffle> (per-chain "
+                        "CG, one 64-thread CTA per chain, 4 CTAs/SM)",
                  dram_per_site=(33.589504e6 + 8.192e3) / (2048 * 256),
                  source="profiles/r01/ncu_full_k_cg_resblk.txt"),
     "cfg4": dict(kernel="k_cg_cluster_tx<64,64,4 CTAs,2x2 sites/thread> (per-chain CG, one "
@@ -96,6 +96,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-stencil", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-compare", action="store_true",
+                    help="skip the cfg3 integrator comparison (five schemes at ~90%% acceptance)")
     ap.add_argument("--streams", type=int, default=1,
                     help="sub-ensembles issued concurrently on separate streams (measured "
                          "slower than 1 on cfg3: 2 -> -6 %%, profiles/r01/README.md)")
@@ -436,6 +438,78 @@ def graph_bench(torch, sw, reps=10):
     return out
 
 
+# BASELINE.json configs[2]: the five schemes it names ("Omelyan 2MN" is the
+# reference's 5stage, "force-gradient" its 5stage-fg) with the smallest outer
+# step count reaching ~90 % acceptance; ladder starts from SURVEY 8(d)'s
+# CPU estimates minus a margin.
+COMPARE_SCHEMES = (("leapfrog", 6), ("5stage", 3), ("5stage-fg", 2), ("nested-fg", 2),
+                   ("adapted-nested-fg", 2))
+COMPARE_TARGET = 0.90
+
+
+def force_evals_per_step(scheme):
+    """Fermion-force evaluations per macro step as the reference executes the
+    program (integrators.py:278-349, no merging of adjacent kicks): a kick
+    is one force, an FG kick a force plus a force-gradient term (two)."""
+    from paper_1512_03812_b200.integrators import PROGRAMS
+    n = 0
+    for name, _ in PROGRAMS[scheme]:
+        if name in ("K", "Kf"):
+            n += 1
+        elif name.startswith("G"):
+            n += 2
+    return n
+
+
+def integrator_comparison(torch, sw, F, q0, drng, reps=2, max_tries=8):
+    """cfg3's integrator comparison on the bench ensemble: for every scheme,
+    the smallest outer step count n (h = tau/n) whose acceptance over the
+    whole ensemble from the common start q0 reaches COMPARE_TARGET, then
+    `reps` timed updates at that n (CUDA events).  Reports chain-traj/s,
+    reference-convention inversions, actual CG solves and CG iterations per
+    chain-trajectory, and force evaluations per trajectory."""
+    from paper_1512_03812_b200.integrators import INVERSIONS_PER_STEP
+    chains = q0.shape[0]
+    out = {"target_acceptance": COMPARE_TARGET, "chains": chains,
+           "start_avg_plaquette": float(sw.avg_plaquette(q0).mean().item()),
+           "micro_per_call": CFG3["micro_per_call"], "schemes": {}}
+    for scheme, n0 in COMPARE_SCHEMES:
+        ladder = []
+        n = n0
+        for _ in range(max_tries):
+            cfg = sw.HmcConfig(h=1.0 / n, **{**CFG3, "scheme": scheme})
+            _, pend = sw.hmc_update_ensemble_async(q0, cfg, drng)
+            acc = float(pend.resolve().accepted.mean())
+            ladder.append([n, acc])
+            if acc >= COMPARE_TARGET:
+                break
+            n += 1
+        cfg = sw.HmcConfig(h=1.0 / n, **{**CFG3, "scheme": scheme})
+        torch.cuda.synchronize()
+        F.CG_PROFILE = []
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q, pends = q0, []
+        e0.record()
+        for _ in range(reps):
+            q, pend = sw.hmc_update_ensemble_async(q, cfg, drng)
+            pends.append(pend)
+        e1.record()
+        torch.cuda.synchronize()
+        sts = [p.resolve() for p in pends]
+        prof, F.CG_PROFILE = F.CG_PROFILE, None
+        ms = e0.elapsed_time(e1) / reps
+        iters = sum(int(it.sum().item()) for _, _, it, _ in prof)
+        out["schemes"][scheme] = {
+            "n_steps": n, "h": 1.0 / n, "acceptance_ladder": ladder,
+            "acceptance": float(np.mean([st.accepted.mean() for st in sts])),
+            "chain_traj_per_s": chains / (ms * 1e-3), "ms_per_update": ms,
+            "inversions_per_traj_reference_convention": INVERSIONS_PER_STEP[scheme] * n,
+            "force_evals_per_traj": force_evals_per_step(scheme) * n,
+            "cg_solves_per_traj": len(prof) / reps,
+            "cg_iterations_per_chain_traj": iters / (chains * reps)}
+    return out
+
+
 def _device_for(local, torch):
     """One GPU per rank.  SCH_DIST_BACKEND=gloo (control-flow tests of the
     multi-rank bench on a 1-GPU box) maps ranks onto the visible devices."""
@@ -528,9 +602,6 @@ def run_ours(args):
             main.wait_stream(stm)
         return pend
 
-    def ensemble_step(qs):
-        return [p.resolve() for p in issue_step(qs)]
-
     def run_steps(n, on_stats=None, ahead=2):
         """n updates with `ahead` steps queued: step k+ahead is issued before
         step k's per-chain results are read back, so a host-side stall (the
@@ -554,8 +625,9 @@ def run_ours(args):
     # (tools/step_jitter.py), so collect once here and keep it off while timing.
     gc.collect()
     gc.disable()
-    for _ in range(args.warmup):
-        sts = ensemble_step(qs)
+    # warm up in the timed region's own pattern (steps queued ahead), so the
+    # caching allocator already holds the buffers of every in-flight step
+    sts = run_steps(args.warmup)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -686,9 +758,11 @@ def run_ours(args):
                "ms_per_step": ems / steps_e2e}
 
     gc.enable()
-    graphs = None
+    graphs = compare = None
     if rank == 0 and not args.no_stencil:
         graphs = graph_bench(torch, sw)
+    if rank == 0 and not args.no_compare and S == 1:
+        compare = integrator_comparison(torch, sw, F, qs[0], drngs[0])
 
     if rank == 0:
         line = {
@@ -735,6 +809,7 @@ def run_ours(args):
             "clocks": clk,
             "stencil": stencil,
             "graph_capture": graphs,
+            "integrators": compare,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

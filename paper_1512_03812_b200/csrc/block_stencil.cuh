@@ -88,4 +88,29 @@ struct SiteBlock {
       if (j == 0) hop_acc<DAG, 3>(out[k], ft[k], false, out[k], 0.0);
     }
   }
+
+  // The same face hops split by direction (the shuffle-exchange kernels add
+  // the t-faces before the exchange barrier, the x-faces after it).
+  template <bool DAG>
+  static SCH_DEV void faces_t(const double2* u1, const double2* ft, Spinor* out) {
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      const int j = k % BT;
+      if (j == BT - 1) hop_acc<DAG, 2>(out[k], cmul(u1[k], ft[k]), false, out[k], 0.0);
+      if (j == 0) hop_acc<DAG, 3>(out[k], ft[k], false, out[k], 0.0);
+    }
+  }
+  template <bool DAG>
+  static SCH_DEV void faces_x(const double2* u0, const double2* fx, Spinor* out) {
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      const int i = k / BT;
+      if (i == BX - 1) hop_acc<DAG, 0>(out[k], cmul(u0[k], fx[k]), false, out[k], 0.0);
+      if (i == 0) hop_acc<DAG, 1>(out[k], fx[k], false, out[k], 0.0);
+    }
+  }
 };
+
+SCH_DEV double2 shfl_d2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}

@@ -58,18 +58,18 @@ int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
-template <int LC, int TC, int BX, int BT, int MINB>
+template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0>
 int launch_resblk(sch_ctx* ctx, const ResArgs& a, int B) {
   constexpr int NT = LC * TC / (BX * BT);
   const size_t smem = sizeof(double2) * 2 * (2 * BT + 2 * BX) * NT;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB>,
+    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB, TSH>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  k_cg_resblk<LC, TC, BX, BT, MINB><<<B, NT, smem, ctx->stream>>>(a);
+  k_cg_resblk<LC, TC, BX, BT, MINB, TSH><<<B, NT, smem, ctx->stream>>>(a);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
@@ -86,8 +86,15 @@ int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
     if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%dx%dx%d", &fnt, &fspt, &fminb, &fspec);
   }
   const bool forced = fnt > 0 && (long long)fnt * fspt >= V;
-  if (!forced && a.L == 16 && a.T == 16) return launch_resblk<16, 16, 2, 2, 4>(ctx, a, B);
-  if (!forced && a.L == 32 && a.T == 32) return launch_resblk<32, 32, 2, 2, 1>(ctx, a, B);
+  static int tsh = -1;   // t-faces through warp shuffles (default; SCH_RESBLK_TSH=0: SMEM)
+  if (tsh < 0) {
+    const char* e = getenv("SCH_RESBLK_TSH");
+    tsh = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (!forced && a.L == 16 && a.T == 16)
+    return tsh ? launch_resblk<16, 16, 2, 2, 4, 1>(ctx, a, B) : launch_resblk<16, 16, 2, 2, 4>(ctx, a, B);
+  if (!forced && a.L == 32 && a.T == 32)
+    return tsh ? launch_resblk<32, 32, 2, 2, 1, 1>(ctx, a, B) : launch_resblk<32, 32, 2, 2, 1>(ctx, a, B);
   int nt, spt, minb;
   bool spec = true;
   if (forced) {

@@ -25,7 +25,13 @@
 
 #include "block_stencil.cuh"
 
-template <int LC, int TC, int BX, int BT, int MINB>
+//
+// TSH = 1 moves the t-direction faces from shared memory to warp shuffles:
+// a block row of NBT = TC/BT threads is contiguous in the thread index, so
+// both t-neighbours of a thread sit in its own warp (NBT divides 32).  The
+// t-face hops are then added before the exchange barrier and only the
+// x-faces go through shared memory (-50 % shared-memory exchange traffic).
+template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0>
 __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs a) {
   using Blk = SiteBlock<BX, BT>;
   constexpr int SPT = Blk::SPT;
@@ -35,6 +41,7 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
   constexpr int NW = NT / 32;
   constexpr int PL = (2 * BT + 2 * BX) * NT;   // double2 per exchange stage
   static_assert(TC % BT == 0 && LC % BX == 0 && NT % 32 == 0, "block shape");
+  static_assert(!TSH || 32 % NBT == 0, "t-neighbours must share a warp");
   // plane offsets inside one stage
   constexpr int O0 = 0, O1 = BT * NT, O2 = 2 * BT * NT, O3 = (2 * BT + BX) * NT;
   extern __shared__ double2 sm[];
@@ -81,13 +88,28 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
 
   // One exchange stage, split around its barrier: exports + interior hops
   // before, face loads + face hops after.
+  const int lane_tp = ttp & 31, lane_tm = ttm & 31;
   auto stage_pre = [&](auto dag, double2* E, const Spinor* v, Spinor* out) {
     constexpr bool DAG = decltype(dag)::value;
+    double2 tf[2][BX];
     Blk::template produce<DAG>(u0, u1, v, [&](int plane, int idx, double2 val) {
       constexpr int off[4] = {O0, O1, O2, O3};
-      E[off[plane] + idx * NT + tid] = val;
+      if (TSH && plane >= 2)
+        tf[plane - 2][idx] = val;
+      else
+        E[off[plane] + idx * NT + tid] = val;
     });
     Blk::template interior<DAG>(u0, u1, v, out, a.diag);
+    if constexpr (TSH) {
+      double2 ft[SPT];
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        const int i = k / BT, j = k % BT;
+        if (j == BT - 1) ft[k] = shfl_d2(tf[0][i], lane_tp);
+        if (j == 0) ft[k] = shfl_d2(tf[1][i], lane_tm);
+      }
+      Blk::template faces_t<DAG>(u1, ft, out);
+    }
   };
   auto stage_post = [&](auto dag, const double2* E, Spinor* out) {
     constexpr bool DAG = decltype(dag)::value;
@@ -97,10 +119,13 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
       const int i = k / BT, j = k % BT;
       if (i == BX - 1) fx[k] = E[O0 + j * NT + txp];
       if (i == 0) fx[k] = E[O1 + j * NT + txm];
-      if (j == BT - 1) ft[k] = E[O2 + i * NT + ttp];
-      if (j == 0) ft[k] = E[O3 + i * NT + ttm];
+      if (!TSH && j == BT - 1) ft[k] = E[O2 + i * NT + ttp];
+      if (!TSH && j == 0) ft[k] = E[O3 + i * NT + ttm];
     }
-    Blk::template faces<DAG>(u0, u1, fx, ft, out);
+    if constexpr (TSH)
+      Blk::template faces_x<DAG>(u0, fx, out);
+    else
+      Blk::template faces<DAG>(u0, u1, fx, ft, out);
   };
   using F = std::integral_constant<bool, false>;
   using T = std::integral_constant<bool, true>;
