@@ -103,6 +103,8 @@ def parse():
                          "slower than 1 on cfg3: 2 -> -6 %%, profiles/r01/README.md)")
     ap.add_argument("--strips", type=int, default=1, help="cfg5: strips on one GPU (local transport)")
     ap.add_argument("--cfg5-size", type=int, default=2048)
+    ap.add_argument("--transport", choices=("local", "nccl", "p2p"), default=None,
+                    help="cfg5 halo/sum transport (default: nccl under torchrun, else local)")
     args = ap.parse_args()
     w = WORKLOADS[args.workload]
     if args.chains is None:
@@ -819,8 +821,9 @@ def run_ours(args):
 
 def run_cfg5(args):
     """BASELINE configs[4]: one 2048x2048 lattice (beta=8, m0=0.05, hot start),
-    x-strip domain decomposition: one strip per rank over NCCL (torchrun), or
-    --strips S strips on one GPU (local transport).  Reports the decomposed
+    x-strip domain decomposition: one strip per rank over NCCL or peer-memory
+    mailboxes (torchrun; --transport nccl|p2p), or --strips S strips on one
+    GPU (local copy-kernel transport, or --transport p2p on local mailboxes).  Reports the decomposed
     fused D^dag D (96 B/site) and the CG to 1e-10 (352 B/site/iteration)."""
     import torch
     import torch.distributed as dist
@@ -837,7 +840,7 @@ def run_cfg5(args):
     rng = np.random.default_rng(5)
     q = rng.uniform(-np.pi, np.pi, (2, L, T))
     psi = rng.standard_normal((L, T, 2)) + 1j * rng.standard_normal((L, T, 2))
-    lat = StripLattice(L, T, strips=None if world > 1 else args.strips)
+    lat = StripLattice(L, T, strips=None if world > 1 else args.strips, transport=args.transport)
     op = DDWilsonDirac(lat, lat.scatter_links(q), 0.05)
     p_ext = lat.scatter_spinor(psi)
     del q, psi
@@ -902,7 +905,7 @@ def run_cfg5(args):
             "dtype": "c128", "data": "synthetic (hot start)",
             "config": {"workload": f"cfg5: one {L}x{T} lattice, m0=0.05, x-strips",
                        "strips": lat.G, "strip_rows": lat.Lloc,
-                       "transport": "nccl" if world > 1 else "local"},
+                       "transport": lat.transport},
             "roofline": {"bound": "hbm", "achieved": gbs / max(world, 1), "peak": hbm_peak,
                          "unit": "GB/s per GPU", "frac": gbs / max(world, 1) / hbm_peak,
                          "peak_kind": peak_kind},

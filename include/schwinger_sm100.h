@@ -180,12 +180,23 @@ int sch_np_metropolis(sch_ctx* ctx, void* state, const double* dh, int* accept, 
  * rows per side) in the usual per-site layouts.  nranks == 1: every strip in
  * this process, halo exchange by a copy kernel.  nranks > 1: one strip per
  * rank, NCCL send/recv of the 2-row faces and NCCL all-reduce of the CG
- * scalars (libnccl.so.2 bound at run time). */
+ * scalars (libnccl.so.2 bound at run time), or — nccl_id NULL, then
+ * sch_dd_p2p_open/_connect — peer-memory mailboxes over NVLink (CUDA IPC).
+ * Replaces nothing in the reference, which has no decomposed path: it is the
+ * multi-GPU form of WilsonDirac.normal / cg_normal (fermion.py:129-217). */
 typedef struct sch_dd sch_dd;
 int sch_nccl_unique_id(sch_ctx* ctx, void* id_out /* 128 bytes */);
 int sch_dd_create(sch_ctx* ctx, const void* nccl_id, int nranks, int rank, int L, int T,
                   int strips_local, sch_dd** out);
 int sch_dd_destroy(sch_dd* dd);
+/* p2p transport, step 1: allocate the zeroed mailboxes of this process's
+ * strips; writes their CUDA IPC handle (64 bytes; zero when nranks == 1) */
+int sch_dd_p2p_open(sch_ctx* ctx, sch_dd* dd, void* ipc_handle_out);
+/* p2p transport, step 2 (after every rank's step 1): map the other ranks'
+ * mailboxes from nranks x 64 handle bytes in rank order and switch the
+ * exchanges and global sums of this dd to peer-memory kernels.  With
+ * nranks == 1 (all strips in this process) the mailbox table is local. */
+int sch_dd_p2p_connect(sch_ctx* ctx, sch_dd* dd, const void* ipc_handles);
 /* out4 = {strips_local, Lloc, Lext, G} */
 int sch_dd_geometry(const sch_dd* dd, int* out4);
 /* refresh the halo rows of a field [S][planes][Lext][T][words_per_site] (doubles) */

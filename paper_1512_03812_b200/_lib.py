@@ -73,6 +73,8 @@ _SIGNATURES = {
     "sch_dd_create": [_c_ptr, _c_ptr, _c_int, _c_int, _c_int, _c_int, _c_int,
                       ctypes.POINTER(_c_ptr)],
     "sch_dd_destroy": [_c_ptr],
+    "sch_dd_p2p_open": [_c_ptr, _c_ptr, _c_ptr],
+    "sch_dd_p2p_connect": [_c_ptr, _c_ptr, _c_ptr],
     "sch_dd_geometry": [_c_ptr, ctypes.POINTER(_c_int)],
     "sch_dd_exchange": [_c_ptr, _c_ptr, _c_ptr, _c_int, _c_int],
     "sch_dd_own_sum": [_c_ptr, _c_ptr, _c_int, _c_ptr, _c_ptr, _c_ptr],

@@ -20,6 +20,23 @@
 //           the +-x neighbours (grouped), ncclAllReduce of the CG scalars.
 //           libnccl.so.2 is bound at run time (dlopen), so the library still
 //           loads on machines without NCCL.
+//   p2p   : peer memory over NVLink, no NCCL on the data path.  Every strip
+//           has a mailbox in its owner's HBM (face slots, arrival / ack
+//           counters, reduction slots and flags); the mailboxes of the other
+//           ranks are mapped with CUDA IPC (sch_dd_p2p_open / _connect).  A
+//           face exchange is a push kernel that stores the strip's two edge
+//           rows straight into the neighbours' mailboxes (NVLink stores) and
+//           bumps their arrival counters with a system-scope release, and a
+//           pull kernel that waits on its own counters and copies the slots
+//           into the halo rows, then acknowledges to the producer (credit for
+//           slot reuse, two slots per side).  A global sum is one kernel that
+//           reduces the strip's partials and stores the value into slot
+//           [strip] of every mailbox with a release flag, and one that waits
+//           for all G flags and sums the G slots in strip order — identical
+//           on every rank, deterministic.  The same kernels serve S strips
+//           held by one process (loopback: mailbox table = local pointers;
+//           every wait is already satisfied by the preceding push in stream
+//           order), which is how the protocol is exercised on one GPU.
 //
 // CG semantics are the reference's (fermion.py:171-217) for a single chain.
 // p and x are updated on halo rows too (from exchanged r and their own
@@ -98,7 +115,17 @@ struct sch_dd {
   int S = 1;                  // strips held by this process
   int G = 1;                  // strips in the whole lattice
   int L = 0, T = 0, Lloc = 0, Lext = 0;
-  ncclComm_t comm = nullptr;  // null => local transport
+  ncclComm_t comm = nullptr;  // null => local transport (unless p2p)
+  // p2p transport (peer-memory mailboxes)
+  bool p2p = false;
+  char* box_mem = nullptr;            // this process's S mailboxes
+  size_t box_bytes = 0;               // one mailbox
+  char** box_tab = nullptr;           // device table: G mailbox pointers
+  std::vector<void*> ipc_opened;      // peer allocations mapped with cudaIpcOpenMemHandle
+  // device counters: [0] exchanges done, [1] global sums done, [2] pull CTAs
+  // finished in the current exchange.  Kept on the device so the kernels
+  // find their sequence number themselves and a CG loop can be captured.
+  unsigned long long* seq_dev = nullptr;
 };
 
 namespace {
@@ -135,8 +162,13 @@ __global__ void k_dd_exchange_local(double* __restrict__ f, int S, int P, int Le
   }
 }
 
+int p2p_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W);
+int p2p_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out);
+
 int dd_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
+  if (dd->p2p) return p2p_exchange(ctx, dd, f, P, W);
   if (dd->comm == nullptr) {
+    if (dd->nranks > 1) return sch_fail(ctx, SCH_ERR_ARG, "dd: no transport (NCCL id or p2p connect)");
     const long long n = (long long)dd->S * P * 4 * dd->T * W;
     unsigned grid = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
     k_dd_exchange_local<<<grid, 256, 0, ctx->stream>>>(f, dd->S, P, dd->Lext, dd->Lloc, dd->T, W);
@@ -161,7 +193,7 @@ int dd_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
   return SCH_OK;
 }
 
-// global sum of n partials (fixed order) into *out, then across ranks
+// global sum of the S*n partials (fixed order) into *out, then across ranks
 __global__ void k_dd_sum(const double* __restrict__ part, int n, double* __restrict__ out) {
   __shared__ double slot[32];
   double acc = 0.0;
@@ -170,11 +202,202 @@ __global__ void k_dd_sum(const double* __restrict__ part, int n, double* __restr
   if (threadIdx.x == 0) *out = s;
 }
 
+// part holds n partials per local strip, [S][n]
 int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out) {
-  k_dd_sum<<<1, 256, 0, ctx->stream>>>(part, n, out);
+  if (dd->p2p) return p2p_allsum(ctx, dd, part, n, out);
+  if (dd->comm == nullptr && dd->nranks > 1)
+    return sch_fail(ctx, SCH_ERR_ARG, "dd: no transport (NCCL id or p2p connect)");
+  k_dd_sum<<<1, 256, 0, ctx->stream>>>(part, dd->S * n, out);
   SCH_LAUNCHED(ctx);
   if (dd->comm != nullptr)
     SCH_NCCL(ctx, nccl().AllReduce(out, out, 1, ncclDouble, ncclSum, dd->comm, ctx->stream));
+  return SCH_OK;
+}
+
+// ------------------------------------------------------ p2p transport
+// Mailbox of one strip (in its owner's HBM), byte offsets from P2PBox:
+//   [0]    u64 arrived[2]   push CTAs that delivered into face side d
+//   [16]   u64 acked[2]     pull CTAs of the neighbour that consumed what
+//                           this strip pushed right (0) / left (1)
+//   [256]  u64 redflag[G]   last global-sum sequence number stored by strip g
+//   [..]   f64 red[2][G]    global-sum slots (two, by sequence parity)
+//   [..]   f64 face[2][2][2*T*kFW]  side (0 = from the left neighbour,
+//                           1 = from the right) x slot (sequence parity) x
+//                           two rows of up to kFW words per site
+constexpr int kFW = 4;          // words per site a face slot holds (P*W <= 4)
+constexpr int kNBuf = 2;        // face / sum slots per side (credit window)
+constexpr int kP2PBlk = 16;     // CTAs per side of a push / pull launch (counting unit)
+constexpr long long kSpinCap = 1ll << 27;   // ~10 s of polling, then trap (no silent hang)
+
+struct P2PGeom {
+  size_t off_redflag, off_red, off_face, bytes;
+  long long slot_words;
+};
+
+P2PGeom p2p_geom(int G, int T) {
+  P2PGeom g;
+  auto al = [](size_t v) { return (v + 255) & ~size_t(255); };
+  g.off_redflag = 256;
+  g.off_red = al(g.off_redflag + sizeof(unsigned long long) * G);
+  g.off_face = al(g.off_red + sizeof(double) * kNBuf * G);
+  g.slot_words = 2ll * T * kFW;
+  g.bytes = al(g.off_face + sizeof(double) * 2 * kNBuf * g.slot_words);
+  return g;
+}
+
+SCH_DEV unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+SCH_DEV void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+SCH_DEV void add_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+SCH_DEV void spin_until(const unsigned long long* p, unsigned long long target) {
+  long long n = 0;
+  while (ld_acquire_sys(p) < target) {
+    __nanosleep(64);
+    if (++n > kSpinCap) __trap();   // a peer never arrived: fail the launch, do not hang
+  }
+}
+
+struct P2PArgs {
+  char* const* tab;   // G mailbox pointers (local or IPC-mapped)
+  unsigned long long* seq;   // sch_dd::seq_dev
+  int strip0, S, G, Lext, Lloc, T;
+  size_t off_redflag, off_red, off_face;
+  long long slot_words;
+};
+
+SCH_DEV unsigned long long* box_u64(const P2PArgs& a, int g, size_t off) {
+  return (unsigned long long*)(a.tab[g] + off);
+}
+
+// grid (kP2PBlk, S, 2): d = 0 pushes rows Lloc, Lloc+1 into the right
+// neighbour's side-0 slot, d = 1 rows 2, 3 into the left neighbour's side-1 slot
+__global__ void k_p2p_push(const double* __restrict__ f, int P, int W, P2PArgs a) {
+  const int s = blockIdx.y, d = blockIdx.z, g = a.strip0 + s;
+  const unsigned long long seq = *(volatile unsigned long long*)a.seq + 1;
+  const int tgt = d == 0 ? (g + 1) % a.G : (g - 1 + a.G) % a.G;
+  if (threadIdx.x == 0 && seq > kNBuf)   // credit: the slot's previous content was consumed
+    spin_until(box_u64(a, g, 16 + 8 * d), (unsigned long long)kP2PBlk * (seq - kNBuf));
+  __syncthreads();
+  double* slot = (double*)(a.tab[tgt] + a.off_face) + (d * kNBuf + seq % kNBuf) * a.slot_words;
+  const long long row = (long long)a.T * W, per_plane = 2 * row;
+  const long long plane = (long long)a.Lext * row;
+  const double* src = f + (long long)s * P * plane + (long long)(d == 0 ? a.Lloc : 2) * row;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P * per_plane;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long pl = i / per_plane, e = i - pl * per_plane;
+    slot[i] = src[pl * plane + e];   // NVLink store when tgt is remote
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    add_release_sys(box_u64(a, tgt, 8 * d), 1ull);
+  }
+}
+
+// grid (kP2PBlk, S, 2): d = 0 fills rows 0, 1 from side 0, d = 1 rows
+// Lloc+2, Lloc+3 from side 1, then returns the credit to the producer
+__global__ void k_p2p_pull(double* __restrict__ f, int P, int W, P2PArgs a) {
+  const int s = blockIdx.y, d = blockIdx.z, g = a.strip0 + s;
+  const unsigned long long seq = *(volatile unsigned long long*)a.seq + 1;
+  const int src_strip = d == 0 ? (g - 1 + a.G) % a.G : (g + 1) % a.G;
+  if (threadIdx.x == 0) spin_until(box_u64(a, g, 8 * d), (unsigned long long)kP2PBlk * seq);
+  __syncthreads();
+  const double* slot = (const double*)(a.tab[g] + a.off_face) + (d * kNBuf + seq % kNBuf) * a.slot_words;
+  const long long row = (long long)a.T * W, per_plane = 2 * row;
+  const long long plane = (long long)a.Lext * row;
+  double* dst = f + (long long)s * P * plane + (long long)(d == 0 ? 0 : a.Lloc + 2) * row;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < P * per_plane;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long pl = i / per_plane, e = i - pl * per_plane;
+    dst[pl * plane + e] = __ldcg(slot + i);   // L2: the peer's stores land there, not in L1
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    add_release_sys(box_u64(a, src_strip, 16 + 8 * d), 1ull);
+    // the last CTA out advances the exchange counter (every CTA has read it)
+    const unsigned long long total = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+    if (atomicAdd(a.seq + 2, 1ull) == total - 1) {
+      a.seq[2] = 0;
+      __threadfence();
+      *(volatile unsigned long long*)a.seq = seq;
+    }
+  }
+}
+
+// one CTA per local strip: the strip's partials (fixed order) -> slot
+// [seq parity][g] of every mailbox, then its flag [g] = seq (release)
+__global__ void k_p2p_red_push(const double* __restrict__ part, int n, P2PArgs a) {
+  __shared__ double slot[32];
+  const unsigned long long seq = *(volatile unsigned long long*)(a.seq + 1) + 1;
+  const int s = blockIdx.x, g = a.strip0 + s;
+  double acc = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) acc += part[(long long)s * n + k];
+  const double v = block_sum_rt(acc, slot);
+  if (threadIdx.x == 0) {
+    for (int h = 0; h < a.G; ++h) ((double*)(a.tab[h] + a.off_red))[(seq % kNBuf) * a.G + g] = v;
+    __threadfence_system();
+    for (int h = 0; h < a.G; ++h) st_release_sys(box_u64(a, h, a.off_redflag) + g, seq);
+  }
+}
+
+// wait for the G contributions of sum `seq` in the first local strip's
+// mailbox, add them in strip order (the same bits on every rank)
+__global__ void k_p2p_red_finish(P2PArgs a, double* __restrict__ out) {
+  const int g0 = a.strip0;
+  const unsigned long long seq = *(volatile unsigned long long*)(a.seq + 1) + 1;
+  for (int h = threadIdx.x; h < a.G; h += blockDim.x) spin_until(box_u64(a, g0, a.off_redflag) + h, seq);
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    const double* red = (const double*)(a.tab[g0] + a.off_red) + (seq % kNBuf) * a.G;
+    double v = 0.0;
+    for (int h = 0; h < a.G; ++h) v += __ldcg(red + h);
+    *out = v;
+  }
+  __syncwarp();
+  if (threadIdx.x == 0) *(volatile unsigned long long*)(a.seq + 1) = seq;   // one warp: all have read it
+}
+
+P2PArgs p2p_args(const sch_dd* dd) {
+  const P2PGeom pg = p2p_geom(dd->G, dd->T);
+  P2PArgs a;
+  a.tab = dd->box_tab;
+  a.seq = dd->seq_dev;
+  a.strip0 = dd->rank * dd->S;
+  a.S = dd->S;
+  a.G = dd->G;
+  a.Lext = dd->Lext;
+  a.Lloc = dd->Lloc;
+  a.T = dd->T;
+  a.off_redflag = pg.off_redflag;
+  a.off_red = pg.off_red;
+  a.off_face = pg.off_face;
+  a.slot_words = pg.slot_words;
+  return a;
+}
+
+int p2p_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
+  if (P * W > kFW) return sch_fail(ctx, SCH_ERR_ARG, "p2p exchange: %d words per site > %d", P * W, kFW);
+  const P2PArgs a = p2p_args(dd);
+  const dim3 grid(kP2PBlk, dd->S, 2);
+  k_p2p_push<<<grid, 256, 0, ctx->stream>>>(f, P, W, a);
+  k_p2p_pull<<<grid, 256, 0, ctx->stream>>>(f, P, W, a);
+  ctx->launches += 2;
+  return SCH_OK;
+}
+
+int p2p_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out) {
+  const P2PArgs a = p2p_args(dd);
+  k_p2p_red_push<<<dd->S, 256, 0, ctx->stream>>>(part, n, a);
+  k_p2p_red_finish<<<1, 32, 0, ctx->stream>>>(a, out);
+  ctx->launches += 2;
   return SCH_OK;
 }
 
@@ -198,10 +421,13 @@ SCH_DEV bool own_row(long long i, int T, int Lext, int lo, int hi) {
 __global__ void k_dd_init(const double2* __restrict__ b, const double2* __restrict__ x0,
                           double2* __restrict__ x, double2* __restrict__ r, double2* __restrict__ p,
                           long long nsites, int T, int Lext, int lo, int hi, double* __restrict__ part) {
+  // grid (gx, S): strip blockIdx.y, partial [strip][blockIdx.x]
   __shared__ double slot[32];
   double acc = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nsites;
-       i += (long long)gridDim.x * blockDim.x) {
+  const long long ns = (long long)Lext * T, s0 = blockIdx.y * ns;
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < ns;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long i = s0 + k;
     Spinor bv = ld256_spinor_nc(b, i);
     Spinor xv;
     if (x0) xv = ld256_spinor_nc(x0, i);
@@ -209,10 +435,10 @@ __global__ void k_dd_init(const double2* __restrict__ b, const double2* __restri
     st256_spinor(x, i, xv);
     st256_spinor(r, i, bv);
     st256_spinor(p, i, bv);
-    if (own_row(i, T, Lext, lo, hi)) acc += spinor_norm2(bv);
+    if (own_row(k, T, Lext, lo, hi)) acc += spinor_norm2(bv);
   }
   double s = block_sum_rt(acc, slot);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = s;
 }
 
 __global__ void k_dd_copy(const double2* __restrict__ src, double2* __restrict__ dst, long long nsites) {
@@ -261,21 +487,23 @@ __global__ void k_dd_update(double2* __restrict__ r, double2* __restrict__ p, do
   const int repl = (st.ctl[3] % kDDReplace) == 0;
   const double al = st.sc[SC_ALPHA], be = st.beta[0];
   double acc = 0.0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nsites;
-       i += (long long)gridDim.x * blockDim.x) {
+  const long long ns = (long long)Lext * T, s0 = blockIdx.y * ns;   // grid (gx, S) as k_dd_init
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < ns;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long i = s0 + k;
     Spinor rv = ld256_spinor(r, i), pv = ld256_spinor(p, i), xv = ld256_spinor(x, i);
     pv = sp_fma(be, pv, rv);
     xv = sp_fma(al, pv, xv);
     st256_spinor(p, i, pv);
     st256_spinor(x, i, xv);
-    if (!repl && own_row(i, T, Lext, lo, hi)) {
+    if (!repl && own_row(k, T, Lext, lo, hi)) {
       rv = sp_fma(-al, ld256_spinor_nc(ap, i), rv);
       st256_spinor(r, i, rv);
       acc += spinor_norm2(rv);
     }
   }
   double s = block_sum_rt(acc, slot);
-  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = s;
 }
 
 __global__ void k_dd_check(DDState st, int S) {
@@ -406,7 +634,7 @@ int sch_dd_create(sch_ctx* ctx, const void* nccl_id, int nranks, int rank, int L
                 "dd_create: bad ranks");
   const int G = nranks * strips_local;
   SCH_CHECK_ARG(ctx, L % G == 0 && L / G >= 2 && T >= 2, "dd_create: L must split into strips of >= 2 rows");
-  SCH_CHECK_ARG(ctx, nranks == 1 || strips_local == 1, "dd_create: NCCL transport holds one strip per rank");
+  SCH_CHECK_ARG(ctx, nranks == 1 || strips_local == 1, "dd_create: multi-rank transports hold one strip per rank");
   sch_dd* dd = new sch_dd();
   dd->nranks = nranks;
   dd->rank = rank;
@@ -416,12 +644,11 @@ int sch_dd_create(sch_ctx* ctx, const void* nccl_id, int nranks, int rank, int L
   dd->T = T;
   dd->Lloc = L / G;
   dd->Lext = dd->Lloc + 2 * kHalo;
-  if (nranks > 1) {
+  if (nranks > 1 && nccl_id != nullptr) {   // NCCL transport (else: p2p, connected later)
     if (!nccl().ok) {
       delete dd;
       return sch_fail(ctx, SCH_ERR_CUDA, "libnccl.so.2 not available");
     }
-    SCH_CHECK_ARG(ctx, nccl_id != nullptr, "dd_create: NCCL id required for nranks > 1");
     ncclUniqueId id;
     memcpy(id.internal, nccl_id, sizeof(id.internal));
     ncclResult_t r = nccl().CommInitRank(&dd->comm, nranks, id, rank);
@@ -437,7 +664,54 @@ int sch_dd_create(sch_ctx* ctx, const void* nccl_id, int nranks, int rank, int L
 int sch_dd_destroy(sch_dd* dd) {
   if (!dd) return SCH_OK;
   if (dd->comm) nccl().CommDestroy(dd->comm);
+  for (void* ptr : dd->ipc_opened) cudaIpcCloseMemHandle(ptr);
+  if (dd->box_tab) cudaFree(dd->box_tab);
+  if (dd->seq_dev) cudaFree(dd->seq_dev);
+  if (dd->box_mem) cudaFree(dd->box_mem);
   delete dd;
+  return SCH_OK;
+}
+
+// p2p transport, step 1: allocate (zeroed) the mailboxes of this process's
+// S strips and return their CUDA IPC handle (64 bytes) for the other ranks.
+int sch_dd_p2p_open(sch_ctx* ctx, sch_dd* dd, void* ipc_handle_out) {
+  SCH_CHECK_ARG(ctx, dd && ipc_handle_out, "dd_p2p_open: bad args");
+  SCH_CHECK_ARG(ctx, !dd->box_mem, "dd_p2p_open: already open");
+  const P2PGeom pg = p2p_geom(dd->G, dd->T);
+  dd->box_bytes = pg.bytes;
+  SCH_CUDA(ctx, cudaMalloc(&dd->box_mem, pg.bytes * dd->S));
+  SCH_CUDA(ctx, cudaMemset(dd->box_mem, 0, pg.bytes * dd->S));
+  SCH_CUDA(ctx, cudaMalloc(&dd->box_tab, sizeof(char*) * dd->G));
+  SCH_CUDA(ctx, cudaMalloc(&dd->seq_dev, 4 * sizeof(unsigned long long)));
+  SCH_CUDA(ctx, cudaMemset(dd->seq_dev, 0, 4 * sizeof(unsigned long long)));
+  cudaIpcMemHandle_t h;
+  memset(&h, 0, sizeof(h));
+  if (dd->nranks > 1) SCH_CUDA(ctx, cudaIpcGetMemHandle(&h, dd->box_mem));
+  memcpy(ipc_handle_out, &h, sizeof(h));
+  SCH_CUDA(ctx, cudaDeviceSynchronize());   // mailboxes zeroed before any peer maps them
+  return SCH_OK;
+}
+
+// p2p transport, step 2: map every other rank's mailboxes (handles: nranks
+// x 64 bytes in rank order, as all-gathered by the host layer) and switch
+// this dd to the p2p transport.  All ranks must have finished step 1.
+int sch_dd_p2p_connect(sch_ctx* ctx, sch_dd* dd, const void* ipc_handles) {
+  SCH_CHECK_ARG(ctx, dd && ipc_handles && dd->box_mem, "dd_p2p_connect: open first");
+  std::vector<char*> tab(dd->G);
+  for (int r = 0; r < dd->nranks; ++r) {
+    char* base = dd->box_mem;
+    if (r != dd->rank) {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, (const char*)ipc_handles + 64 * (size_t)r, sizeof(h));
+      void* ptr = nullptr;
+      SCH_CUDA(ctx, cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+      dd->ipc_opened.push_back(ptr);
+      base = (char*)ptr;
+    }
+    for (int s = 0; s < dd->S; ++s) tab[r * dd->S + s] = base + s * dd->box_bytes;
+  }
+  SCH_CUDA(ctx, cudaMemcpy(dd->box_tab, tab.data(), sizeof(char*) * dd->G, cudaMemcpyHostToDevice));
+  dd->p2p = true;
   return SCH_OK;
 }
 
@@ -523,7 +797,8 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   st.ctl = (int*)take(sizeof(int) * 8);
   cudaStream_t s = ctx->stream;
   const int lo = kHalo, hi = kHalo + dd->Lloc;
-  const unsigned egrid = kRedGrid;
+  const dim3 egrid(std::max(1, kRedGrid / dd->S), dd->S);   // elementwise passes: [S][gx] partials
+  const int gx = (int)egrid.x;
 
   // init: b (and x0) halos, then x, r, p on every row
   if ((rc = dd_exchange(ctx, dd, b_ext, 1, 4))) return rc;
@@ -531,7 +806,7 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   k_dd_init<<<egrid, 256, 0, s>>>((const double2*)b_ext, (const double2*)x0_ext, (double2*)x_ext, r, p,
                                   nsites, dd->T, dd->Lext, lo, hi, part_a);
   SCH_LAUNCHED(ctx);
-  if ((rc = dd_allsum(ctx, dd, part_a, egrid, st.sc + SC_NORMB2))) return rc;
+  if ((rc = dd_allsum(ctx, dd, part_a, gx, st.sc + SC_NORMB2))) return rc;
   TileArgs base = dd_tile_args(dd, sh, (const double2*)U_ext, m0);
   if (x0_ext) {   // r = b - A x0 on own rows, then p = r, both with fresh halos
     TileArgs tx = base;
@@ -541,9 +816,9 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
     tx.partial = part_b;
     launch_normal_tile<MODE_X>(sh, tx, s);
     SCH_LAUNCHED(ctx);
-    if ((rc = dd_allsum(ctx, dd, part_b, ntile_part, st.sc + SC_RR))) return rc;
+    if ((rc = dd_allsum(ctx, dd, part_b, tpc, st.sc + SC_RR))) return rc;
     if ((rc = dd_exchange(ctx, dd, (double*)r, 1, 4))) return rc;
-    k_dd_copy<<<egrid, 256, 0, s>>>(r, p, nsites);
+    k_dd_copy<<<egrid.x * egrid.y, 256, 0, s>>>(r, p, nsites);
     SCH_LAUNCHED(ctx);
   }
   k_dd_ctrl_init<<<1, 1, 0, s>>>(st, dd->S, tol, x0_ext != nullptr);
@@ -572,17 +847,17 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
       if ((e = dd_exchange(ctx, dd, (double*)r, 1, 4))) break;
       launch_normal_tile<MODE_P>(sh, tp, q);
       ctx->launches++;
-      if ((e = dd_allsum(ctx, dd, part_a, ntile_part, st.sc + SC_PAP))) break;
+      if ((e = dd_allsum(ctx, dd, part_a, tpc, st.sc + SC_PAP))) break;
       k_dd_alpha<<<1, 1, 0, q>>>(st);
       k_dd_update<<<egrid, 256, 0, q>>>(r, p, (double2*)x_ext, ap, st, nsites, dd->T, dd->Lext, lo,
                                         hi, part_b);
       ctx->launches += 2;
-      if ((e = dd_allsum(ctx, dd, part_b, egrid, st.sc + SC_RR))) break;
+      if ((e = dd_allsum(ctx, dd, part_b, gx, st.sc + SC_RR))) break;
       k_dd_check<<<1, 1, 0, q>>>(st, dd->S);
       // x halos are current (x is updated on every row), so no exchange here
       launch_normal_tile<MODE_X>(sh, txx, q);
       ctx->launches += 2;
-      if ((e = dd_allsum(ctx, dd, part_b, ntile_part, st.sc + SC_TN2))) break;
+      if ((e = dd_allsum(ctx, dd, part_b, tpc, st.sc + SC_TN2))) break;
       k_dd_final<<<1, 1, 0, q>>>(st, dd->S, maxiter);
       k_dd_iter_inc<<<1, 1, 0, q>>>(st);
       ctx->launches += 2;
@@ -594,9 +869,10 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   };
 
   if (dd->comm == nullptr && use_cg_graph() && use_cg_while()) {
-    // local transport: the whole loop on the device (conditional WHILE graph
-    // node, as the streaming engine in cg.cu); NCCL transports keep the
-    // host-driven loop below
+    // local and p2p transports: the whole loop on the device (conditional
+    // WHILE graph node, as the streaming engine in cg.cu; the p2p kernels
+    // keep their sequence numbers on the device); the NCCL transport keeps
+    // the host-driven loop below
     if (!ctx->cap_stream)
       SCH_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
     cudaGraph_t graph;

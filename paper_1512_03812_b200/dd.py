@@ -12,6 +12,11 @@ the C library (csrc/dd.cu):
 * NCCL — ``StripLattice(L, T, group=pg)`` under ``torch.distributed`` with one
   strip per rank; faces go over ``ncclSend/ncclRecv`` to the +-x neighbour
   ranks and the CG scalars over ``ncclAllReduce``.
+* p2p — ``transport="p2p"``: peer-memory mailboxes (csrc/dd.cu): push kernels
+  store faces and reduction partials straight into the neighbours' HBM over
+  NVLink (CUDA IPC mappings exchanged once through ``torch.distributed``),
+  pull / finish kernels wait on release/acquire counters.  With every strip
+  in one process (``strips=G``) the same kernels run on local mailboxes.
 
 The periodic stencil kernels run unchanged on the extended strip; rows
 outside the own range are masked out of outputs and reductions.
@@ -41,14 +46,47 @@ def halo_plan(rank: int, world: int, lloc: int):
             (left, 2, 2, "send"), (right, lloc + 2, 2, "recv")]
 
 
-class StripLattice:
-    """Geometry + C-side handle of an L x T lattice split into x-strips."""
+IPC_HANDLE_BYTES = 64
 
-    def __init__(self, L: int, T: int, strips: int | None = None, group=None):
+
+def allgather_handles(handle: bytes, group=None) -> bytes:
+    """Every rank's 64-byte mailbox handle, concatenated in rank order (what
+    sch_dd_p2p_connect takes)."""
+    if len(handle) != IPC_HANDLE_BYTES:
+        raise ValueError(f"IPC handle must be {IPC_HANDLE_BYTES} bytes, got {len(handle)}")
+    if not (dist.is_initialized() and dist.get_world_size(group) > 1):
+        return bytes(handle)
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, bytes(handle), group=group)
+    return b"".join(out)
+
+
+TRANSPORTS = ("local", "nccl", "p2p")
+
+
+class StripLattice:
+    """Geometry + C-side handle of an L x T lattice split into x-strips.
+
+    ``transport``: "local" (all strips here, copy-kernel halos), "nccl" (one
+    strip per rank) or "p2p" (peer-memory mailboxes; one strip per rank, or
+    all strips here).  Default: "nccl" under a multi-rank process group,
+    else "local"."""
+
+    def __init__(self, L: int, T: int, strips: int | None = None, group=None,
+                 transport: str | None = None):
         self.L, self.T = int(L), int(T)
-        use_nccl = group is not None or (strips is None and dist.is_initialized()
-                                         and dist.get_world_size() > 1)
-        if use_nccl:
+        multi = group is not None or (strips is None and dist.is_initialized()
+                                      and dist.get_world_size() > 1)
+        if transport is None:
+            transport = "nccl" if multi else "local"
+        if transport not in TRANSPORTS:
+            raise ValueError(f"unknown transport {transport!r}; valid: {', '.join(TRANSPORTS)}")
+        if transport == "nccl" and not multi:
+            raise ValueError("the NCCL transport needs a multi-rank process group")
+        if transport == "local" and multi:
+            raise ValueError("the local transport keeps every strip in one process")
+        self.transport = transport
+        if multi:
             self.world = dist.get_world_size(group)
             self.rank = dist.get_rank(group)
             self.local = 1
@@ -56,7 +94,7 @@ class StripLattice:
             self.world, self.rank, self.local = 1, 0, int(strips or 1)
         ctx = _lib.ctx()
         nid = None
-        if self.world > 1:
+        if self.world > 1 and transport == "nccl":
             buf = ctypes.create_string_buffer(128)
             if self.rank == 0:
                 ctx.call("sch_nccl_unique_id", ctypes.cast(buf, ctypes.c_void_p))
@@ -71,6 +109,14 @@ class StripLattice:
         _lib.load().sch_dd_geometry(handle, geo)
         self.S, self.Lloc, self.Lext, self.G = (int(v) for v in geo)
         self.strip0 = self.rank * self.local     # global index of the first local strip
+        if transport == "p2p":
+            h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+            ctx.call("sch_dd_p2p_open", handle, ctypes.cast(h, ctypes.c_void_p))
+            if self.world > 1:
+                dist.barrier(group=group)   # every mailbox zeroed before anyone maps it
+            allh = allgather_handles(h.raw, group)
+            buf = ctypes.create_string_buffer(allh, len(allh))
+            ctx.call("sch_dd_p2p_connect", handle, ctypes.cast(buf, ctypes.c_void_p))
 
     def __del__(self):
         h = getattr(self, "_handle", None)

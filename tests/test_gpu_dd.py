@@ -16,15 +16,16 @@ def npy(t):
     return t.detach().cpu().numpy()
 
 
+@pytest.mark.parametrize("transport", ["local", "p2p"])
 @pytest.mark.parametrize("L,T,G", [(64, 32, 4), (32, 128, 2), (48, 16, 6), (16, 8, 8)])
-def test_dd_normal_and_cg_match_single_lattice(L, T, G):
+def test_dd_normal_and_cg_match_single_lattice(L, T, G, transport):
     import paper_1512_03812_b200 as sw
     from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice
     from oracle import schwinger_oracle as O
     rng = np.random.default_rng(L + T + G)
     q = rng.uniform(-np.pi, np.pi, (2, L, T))
     psi = rng.standard_normal((L, T, 2)) + 1j * rng.standard_normal((L, T, 2))
-    lat = StripLattice(L, T, strips=G)
+    lat = StripLattice(L, T, strips=G, transport=transport)
     assert (lat.S, lat.Lloc, lat.Lext) == (G, L // G, L // G + 4)
     op = DDWilsonDirac(lat, lat.scatter_links(q), 0.1)
     ref = O.normal_op(O.fermion_links(q), psi, 0.1)
@@ -70,10 +71,11 @@ def test_dd_hmc_update_matches_reference_full_lattice(scheme, h, G):
     assert np.max(np.abs(npy(lat.gather_links(q_ext)) - qo)) < 1e-8
 
 
-def test_dd_exchange_fills_halos_from_neighbours():
+@pytest.mark.parametrize("transport", ["local", "p2p"])
+def test_dd_exchange_fills_halos_from_neighbours(transport):
     from paper_1512_03812_b200.dd import StripLattice
     L, T, G = 24, 8, 3
-    lat = StripLattice(L, T, strips=G)
+    lat = StripLattice(L, T, strips=G, transport=transport)
     full = torch.arange(L * T * 4, dtype=torch.float64, device="cuda").reshape(L, T, 2, 2)
     psi = torch.view_as_complex(full.contiguous())
     ext = lat.scatter_spinor(psi)
@@ -107,3 +109,67 @@ def test_dd_cg_zero_rhs_warm_start_and_cap():
     assert rel_err(npy(lat.gather_spinor(x)), xo) < 1e-9
     with pytest.raises(sw.SolverError):
         op.cg(lat.scatter_spinor(b), 1e-12, maxiter=3)
+
+
+@pytest.mark.parametrize("G", [1, 2, 5])
+def test_p2p_mailboxes_over_many_exchanges_and_shapes(G):
+    """The peer-memory transport (mailbox slots reused by sequence parity,
+    credits returned by the pull kernels) on every strip of one process:
+    links (2 planes x 1 word) and spinors (1 x 4) interleaved many times,
+    each exchange == the copy-kernel transport's halos."""
+    from paper_1512_03812_b200.dd import StripLattice
+    L, T = 8 * G, 12
+    a = StripLattice(L, T, strips=G, transport="p2p")
+    b = StripLattice(L, T, strips=G, transport="local")
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(G)
+    for k in range(7):
+        q = torch.rand((2, L, T), dtype=torch.float64, device="cuda", generator=gen)
+        psi = torch.randn((L, T, 2), dtype=torch.complex128, device="cuda", generator=gen)
+        for field, planes, words in ((b.scatter_links(q), 2, 1), (b.scatter_spinor(psi), 1, 4)):
+            want = field.clone()
+            x = field.clone()
+            axis = 1 if planes == 1 else 2   # the extended row axis
+            x.narrow(axis, 0, 2).zero_()
+            x.narrow(axis, a.Lext - 2, 2).zero_()
+            y = x.clone()
+            a.exchange(x, planes, words)
+            b.exchange(y, planes, words)
+            assert torch.equal(x, y) and torch.equal(x, want)
+
+
+def test_p2p_rejects_wide_sites_and_bad_transport():
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200.dd import StripLattice
+    lat = StripLattice(16, 8, strips=2, transport="p2p")
+    f = torch.zeros((2, 3, lat.Lext, 8, 2), dtype=torch.float64, device="cuda")
+    with pytest.raises(Exception):
+        lat.exchange(f, 3, 2)
+    with pytest.raises(ValueError):
+        StripLattice(16, 8, strips=2, transport="nccl")
+    with pytest.raises(ValueError):
+        StripLattice(16, 8, strips=2, transport="udp")
+
+
+def test_dd_hmc_update_p2p_transport_matches_reference():
+    """One scheme end to end on the peer-memory transport (faces after every
+    drift, forces, CG exchanges and sums all through the mailboxes)."""
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200.dd import StripLattice
+    from paper_1512_03812_b200.dd_hmc import dd_hmc_update
+    from oracle import schwinger_oracle as O
+    L, G = 16, 4
+    kw = dict(L=L, T=L, beta=2.0, m0=0.1, tau=1.0, h=0.25, scheme="adapted-nested-fg",
+              micro_per_call=2, cg_tol=1e-10)
+    cfg, ocfg = sw.HmcConfig(**kw), O.Config(**kw)
+    lat = StripLattice(L, L, strips=G, transport="p2p")
+    rng_g, rng_o = O.make_rng(9, 0), O.make_rng(9, 0)
+    q0 = O.hot_start(rng_g, L, L)
+    O.hot_start(rng_o, L, L)
+    q_ext, qo = lat.scatter_links(q0), q0
+    for _ in range(2):
+        q_ext, s = dd_hmc_update(lat, q_ext, cfg, rng_g)
+        qo, so = O.hmc_update(qo, ocfg, rng_o)
+        assert abs(s.dh - so["dh"]) < 1e-8
+        assert s.accepted == so["accepted"] and s.inversions == so["inversions"]
+    assert np.max(np.abs(npy(lat.gather_links(q_ext)) - qo)) < 1e-8

@@ -118,3 +118,33 @@ def test_gather_observables_world2_gloo(total):
         assert np.allclose(obs["dh"], 0.01 * np.arange(total))
         s = summarize(obs)
         assert abs(s["acceptance"] - np.mean(np.arange(total) % 3 != 0)) < 1e-15
+
+
+def _handles_worker(rank, world, port, out_q):
+    from paper_1512_03812_b200.dd import IPC_HANDLE_BYTES, allgather_handles
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = bytes([rank + 1]) * IPC_HANDLE_BYTES
+        out_q.put((rank, allgather_handles(mine)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_p2p_ipc_handles_allgather_rank_order_gloo(world):
+    """The p2p transport's one host-side collective: every rank ends up with
+    all mailbox handles in rank order (the layout sch_dd_p2p_connect maps)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_handles_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = b"".join(bytes([r + 1]) * 64 for r in range(world))
+    assert all(v == want for v in res.values())
