@@ -49,8 +49,9 @@ FALLBACK_HBM = 6650.0
 # The dominant kernel of each ensemble workload, and the DRAM bytes per
 # lattice site of one of its launches measured by ncu --set full (U and b
 # in, x out — the solve itself stays on chip):
-#   cfg3: profiles/r01/ncu_full_k_cg_resblk.txt, 33.589504 MB read + 8.192 KB
-#         written for 2048 chains x 256 sites
+#   cfg3: profiles/r01/ncu_full_k_cg_resblk_tsh.txt, 134.307328 MB read +
+#         36.36352 MB written for 8192 chains x 256 sites (x leaves partly
+#         through L2 after the kernel ends); FP64 pipe 70.1 % active
 #   cfg4: profiles/r01/ncu_full_k_cg_cluster.txt, 268.8832 MB read +
 #         103.359744 MB written for 1024 chains x 4096 sites (b is re-read by
 #         the true-residual checks; part of it misses L2)
@@ -58,12 +59,14 @@ DRAM_CFG4 = (268.8832e6 + 103.359744e6) / (1024 * 4096)
 CG_KERNELS = {
     "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread,t-faces by warp shuffle> (per-chain "
                         "CG, one 64-thread CTA per chain, 4 CTAs/SM)",
-                 dram_per_site=(33.589504e6 + 8.192e3) / (2048 * 256),
-                 source="profiles/r01/ncu_full_k_cg_resblk.txt"),
+                 dram_per_site=(134.307328e6 + 36.36352e6) / (8192 * 256),
+                 fp64_pipe_active=0.701,
+                 source="profiles/r01/ncu_full_k_cg_resblk_tsh.txt"),
     "cfg4": dict(kernel="k_cg_cluster_tx<64,64,4 CTAs,2x2 sites/thread> (per-chain CG, one "
                         "4-CTA cluster per chain, faces and partial sums pushed with st.async "
                         "onto the receiver's mbarrier)",
                  dram_per_site=DRAM_CFG4,
+                 fp64_pipe_active=0.431,
                  source="profiles/r01/ncu_full_k_cg_cluster.txt"),
 }
 
@@ -804,6 +807,10 @@ def run_ours(args):
                          "fp64_tflops": cg_flops / (cg_ms * 1e-3) / 1e12,
                          "fp64_peak_tflops_probe": fp64_peak,
                          "fp64_frac": cg_flops / (cg_ms * 1e-3) / 1e12 / fp64_peak,
+                         "fp64_pipe_active_ncu": CG_KERNELS[args.workload]["fp64_pipe_active"],
+                         "fp64_note": "fp64_frac counts the 152 flop/site model; the kernel "
+                                      "issues ~112 FP64 instructions per site-iteration, and "
+                                      "ncu's FP64 pipe-active fraction is the issue-rate bound",
                          "cg_share_of_step": cg_ms / ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
