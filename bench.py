@@ -215,6 +215,32 @@ def cpu_baseline(seconds, outer):
                       "oracle/schwinger_oracle.py"}
 
 
+# BASELINE.json configs[0] ("cfg1"): the reference's own CPU run, one chain
+CFG1 = dict(L=16, T=16, beta=2.0, m0=0.1, tau=1.0, h=0.2, scheme="adapted-nested-fg",
+            micro_per_call=2, cg_tol=1e-10)
+
+
+def _cpu_cfg1_worker(n_traj):
+    """cfg1 exactly as the reference runs it: hot_start(make_rng(0, 0)), then
+    hmc_update on the same generator, one core."""
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import schwinger_oracle as O
+    cfg = O.Config(**CFG1)
+    rng = O.make_rng(0, 0)
+    q = O.hot_start(rng, cfg.L, cfg.T)
+    t0 = time.perf_counter()
+    for _ in range(n_traj):
+        q, _ = O.hmc_update(q, cfg, rng)
+    return (time.perf_counter() - t0) / n_traj
+
+
+def cpu_cfg1(n_traj=3):
+    with mp.get_context("fork").Pool(1) as pool:
+        sec = pool.apply(_cpu_cfg1_worker, (n_traj,))
+    return {"s_per_trajectory": sec, "cores": 1, "kind": "port",
+            "sample": f"first {n_traj} of cfg1's 20 trajectories (oracle/schwinger_oracle.py)"}
+
+
 def _cpu_stencil_worker(args):
     """Oracle D^dag D on a slice of cfg2 (B_slice x 32^2) for ~seconds."""
     seed, nb, seconds = args
@@ -408,6 +434,33 @@ def stencil_bench(torch, sw, _lib, hbm_peak):
     return res
 
 
+def cfg1_bench(torch, sw, cpu=None, n_traj=20):
+    """BASELINE configs[0] on the GPU: the single chain of the reference's CPU
+    run (hot start from make_rng(0, 0), 20 trajectories, h = 0.2), each
+    update one replay of a captured CUDA graph; beside the CPU port's
+    seconds per trajectory on one core."""
+    cfg = sw.HmcConfig(**CFG1)
+    d = sw.NumpyDeviceRng(seed=0, n_chains=1, stream0=0)
+    q = d.hot_start(sw.LatticeGeom(cfg.L, cfg.T))
+    upd = sw.EnsembleUpdateGraph(q, cfg, d)
+    upd.step()   # capture + first trajectory (untimed)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(n_traj):
+        upd.step()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n_traj
+    out = {"workload": "cfg1: one 16x16 chain, beta=2, m0=0.1, adapted-nested-fg 5x2 (h=0.2), "
+                       "tol 1e-10, hot start make_rng(0, 0)",
+           "gpu_ms_per_trajectory": ms, "trajectories": n_traj}
+    if cpu is not None:
+        out["cpu"] = cpu
+        out["speedup_vs_1_core"] = cpu["s_per_trajectory"] * 1e3 / ms
+    return out
+
+
 def graph_bench(torch, sw, reps=10):
     """Small ensembles are launch-bound: one HMC update (cfg3 physics) per
     step eagerly vs replayed as one captured CUDA graph (EnsembleUpdateGraph)."""
@@ -548,11 +601,13 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     hbm_peak, peak_kind = peaks()
 
-    cpu = cpu_stencil = None
+    cpu = cpu_stencil = cpu1 = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.cpu_seconds, args.outer)   # before CUDA init (fork-safe)
         if not args.no_stencil:
             cpu_stencil = cpu_stencil_baseline(min(args.cpu_seconds, 5.0))
+            if args.workload == "cfg3":
+                cpu1 = cpu_cfg1()
 
     local = _device_for(local, torch)
     torch.cuda.set_device(local)
@@ -763,9 +818,11 @@ def run_ours(args):
                "ms_per_step": ems / steps_e2e}
 
     gc.enable()
-    graphs = compare = None
+    graphs = compare = single = None
     if rank == 0 and not args.no_stencil:
         graphs = graph_bench(torch, sw)
+        if args.workload == "cfg3":
+            single = cfg1_bench(torch, sw, cpu1)
     if rank == 0 and not args.no_compare and S == 1:
         compare = integrator_comparison(torch, sw, F, qs[0], drngs[0])
 
@@ -819,6 +876,7 @@ def run_ours(args):
             "stencil": stencil,
             "graph_capture": graphs,
             "integrators": compare,
+            "cfg1_single_chain": single,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -826,12 +884,33 @@ def run_ours(args):
     return 0
 
 
+def _cpu_cfg5_worker(L):
+    """one oracle D^dag D on the whole L x L lattice and five
+    CG iterations (one core); the trajectory is extrapolated from them."""
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import schwinger_oracle as O
+    rng = np.random.default_rng(5)
+    U = O.fermion_links(rng.uniform(-np.pi, np.pi, (2, L, L)))
+    psi = rng.standard_normal((L, L, 2)) + 1j * rng.standard_normal((L, L, 2))
+    t0 = time.perf_counter()
+    O.normal_op(U, psi, 0.05)
+    t_op = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    try:
+        O.cg_normal(U, 0.05, psi, 1e-10, maxiter=5)
+    except O.OracleSolverError:
+        pass
+    return t_op, (time.perf_counter() - t0) / 5
+
+
 def run_cfg5(args):
     """BASELINE configs[4]: one 2048x2048 lattice (beta=8, m0=0.05, hot start),
     x-strip domain decomposition: one strip per rank over NCCL or peer-memory
     mailboxes (torchrun; --transport nccl|p2p), or --strips S strips on one
-    GPU (local copy-kernel transport, or --transport p2p on local mailboxes).  Reports the decomposed
-    fused D^dag D (96 B/site) and the CG to 1e-10 (352 B/site/iteration)."""
+    GPU (local copy-kernel transport, or --transport p2p on local mailboxes).
+    Reports the decomposed fused D^dag D (96 B/site), the CG to 1e-10
+    (352 B/site/iteration) and one trajectory, with the CPU port's D^dag D and
+    CG iteration on one core beside them (the CPU trajectory extrapolated)."""
     import torch
     import torch.distributed as dist
 
@@ -839,6 +918,10 @@ def run_cfg5(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     hbm_peak, peak_kind = peaks()
+    cpu5 = None
+    if rank == 0 and world == 1 and not args.no_cpu:   # before CUDA init (fork-safe)
+        with mp.get_context("fork").Pool(1) as pool:
+            cpu5 = pool.apply(_cpu_cfg5_worker, (args.cfg5_size,))
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -923,7 +1006,15 @@ def run_cfg5(args):
                            "ms": traj_ms, "trajectories_per_s": 1e3 / traj_ms, "dh": traj.dh,
                            "inversions": traj.inversions,
                            "includes": "host heatbath draws of the full lattice (reference "
-                                       "generator), H at both ends, Metropolis"}}), flush=True)
+                                       "generator), H at both ends, Metropolis"},
+            "cpu_baseline": None if cpu5 is None else {
+                "ddagd_GBs": 96.0 * sites / cpu5[0] / 1e9, "cg_s_per_iteration": cpu5[1],
+                "trajectory_s_extrapolated": cpu5[1] * iters * traj.inversions / 2,
+                "cores": 1, "kind": "port",
+                "sample": "one oracle D^dag D and 5 CG iterations on the whole lattice; the "
+                          "trajectory = CPU s/iteration x this run's CG iterations of one solve "
+                          "x the trajectory's solves (inversions / 2) — an extrapolation"}}),
+              flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
