@@ -130,6 +130,103 @@ struct sch_dd {
 
 namespace {
 
+// ------------------------------------------------------------- CG state
+struct DDState {
+  double* sc;   // scalars: see SC_* below
+  int* flag;    // [S] need_x (X pass) per local strip (all equal)
+  double* beta; // [S] beta per local strip (all equal)
+  int* ctl;     // [0] done, [1] iters, [2] status, [3] current iteration (device-side loop)
+};
+enum { SC_NORMB2 = 0, SC_PAP, SC_RR, SC_TN2, SC_RS, SC_RSNEW, SC_ALPHA, SC_NORMB, SC_TARGET,
+       SC_BEST, SC_RELRES, SC_COUNT };
+
+SCH_DEV bool own_row(long long i, int T, int Lext, int lo, int hi) {
+  const int row = (int)((i / T) % Lext);
+  return row >= lo && row < hi;
+}
+
+
+// Scalar control of the decomposed CG (fermion.py:171-217), run by one
+// thread right after the global sum it needs — fused into the sum's kernel
+// (local and p2p transports) or a 1-thread kernel after the NCCL all-reduce.
+SCH_DEV void dd_alpha(DDState st) {
+  if (st.ctl[0]) return;
+  const double den = st.sc[SC_PAP];
+  st.sc[SC_ALPHA] = den > 0.0 ? st.sc[SC_RS] / den : 0.0;
+}
+
+SCH_DEV void dd_check(DDState st, int S) {
+  if (st.ctl[0]) return;
+  const int repl = (st.ctl[3] % kDDReplace) == 0;
+  int need;
+  if (repl) {
+    need = 1;
+  } else {
+    const double rsn = st.sc[SC_RR];
+    st.sc[SC_RSNEW] = rsn;
+    need = sqrt(rsn) <= st.sc[SC_TARGET];
+  }
+  for (int s = 0; s < S; ++s) st.flag[s] = need;
+}
+
+SCH_DEV void dd_final(DDState st, int S, int maxiter) {
+  if (st.ctl[0]) return;
+  const int it = st.ctl[3];
+  const int nx = st.flag[0];
+  double rs_new = st.sc[SC_RSNEW];
+  if (nx) {
+    const double tn2 = st.sc[SC_TN2];
+    const double tn = sqrt(tn2);
+    const int repl = (it % kDDReplace) == 0;
+    if (!repl || tn <= st.sc[SC_TARGET]) st.sc[SC_BEST] = tn / st.sc[SC_NORMB];
+    if (tn <= st.sc[SC_TARGET]) {
+      st.ctl[0] = 1;
+      st.ctl[1] = it;
+      st.sc[SC_RELRES] = tn / st.sc[SC_NORMB];
+      for (int s = 0; s < S; ++s) st.flag[s] = 0;
+      return;
+    }
+    rs_new = tn2;
+  }
+  const double rs = st.sc[SC_RS];
+  const double beta = rs > 0.0 ? rs_new / rs : 0.0;
+  for (int s = 0; s < S; ++s) {
+    st.beta[s] = beta;
+    st.flag[s] = 0;
+  }
+  st.sc[SC_RS] = rs_new;
+  if (it >= maxiter) {
+    st.ctl[0] = 1;
+    st.ctl[1] = it;
+    st.ctl[2] = 1;
+    st.sc[SC_RELRES] = fmin(st.sc[SC_BEST], sqrt(rs_new) / st.sc[SC_NORMB]);
+  }
+}
+
+enum { POST_NONE = 0, POST_ALPHA, POST_CHECK, POST_FINAL };
+struct DDPost {
+  int kind = POST_NONE;
+  DDState st{};
+  int S = 1, maxiter = 0;
+  int set_cond = 0;                    // POST_FINAL inside the WHILE graph: drive its condition
+  cudaGraphConditionalHandle h = 0;
+};
+
+SCH_DEV void dd_post_run(const DDPost& p) {
+  if (p.kind == POST_ALPHA) {
+    dd_alpha(p.st);
+  } else if (p.kind == POST_CHECK) {
+    dd_check(p.st, p.S);
+  } else if (p.kind == POST_FINAL) {
+    dd_final(p.st, p.S, p.maxiter);
+    ++p.st.ctl[3];
+    if (p.set_cond)   // iterate while not done (and below the cap)
+      cudaGraphSetConditional(p.h, (p.st.ctl[0] == 0 && p.st.ctl[3] <= p.maxiter) ? 1u : 0u);
+  }
+}
+
+__global__ void k_dd_post(DDPost p) { dd_post_run(p); }
+
 // ---------------------------------------------------------- halo exchange
 // Field layout [S][P planes][Lext][T][W doubles]; copy the 4 halo rows of
 // every strip from its periodic neighbours (local transport).
@@ -163,7 +260,7 @@ __global__ void k_dd_exchange_local(double* __restrict__ f, int S, int P, int Le
 }
 
 int p2p_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W);
-int p2p_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out);
+int p2p_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out, const DDPost& post);
 
 int dd_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
   if (dd->p2p) return p2p_exchange(ctx, dd, f, P, W);
@@ -194,23 +291,33 @@ int dd_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
 }
 
 // global sum of the S*n partials (fixed order) into *out, then across ranks
-__global__ void k_dd_sum(const double* __restrict__ part, int n, double* __restrict__ out) {
+__global__ void k_dd_sum(const double* __restrict__ part, int n, double* __restrict__ out, DDPost post) {
   __shared__ double slot[32];
   double acc = 0.0;
   for (int k = threadIdx.x; k < n; k += blockDim.x) acc += part[k];
   double s = block_sum_rt(acc, slot);
-  if (threadIdx.x == 0) *out = s;
+  if (threadIdx.x == 0) {
+    *out = s;
+    dd_post_run(post);
+  }
 }
 
 // part holds n partials per local strip, [S][n]
-int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out) {
-  if (dd->p2p) return p2p_allsum(ctx, dd, part, n, out);
+// part holds n partials per local strip, [S][n]; `post` runs on the sum
+int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out,
+              const DDPost& post = DDPost{}) {
+  if (dd->p2p) return p2p_allsum(ctx, dd, part, n, out, post);
   if (dd->comm == nullptr && dd->nranks > 1)
     return sch_fail(ctx, SCH_ERR_ARG, "dd: no transport (NCCL id or p2p connect)");
-  k_dd_sum<<<1, 256, 0, ctx->stream>>>(part, dd->S * n, out);
+  k_dd_sum<<<1, 256, 0, ctx->stream>>>(part, dd->S * n, out, dd->comm ? DDPost{} : post);
   SCH_LAUNCHED(ctx);
-  if (dd->comm != nullptr)
+  if (dd->comm != nullptr) {
     SCH_NCCL(ctx, nccl().AllReduce(out, out, 1, ncclDouble, ncclSum, dd->comm, ctx->stream));
+    if (post.kind != POST_NONE) {
+      k_dd_post<<<1, 1, 0, ctx->stream>>>(post);
+      SCH_LAUNCHED(ctx);
+    }
+  }
   return SCH_OK;
 }
 
@@ -350,7 +457,7 @@ __global__ void k_p2p_red_push(const double* __restrict__ part, int n, P2PArgs a
 
 // wait for the G contributions of sum `seq` in the first local strip's
 // mailbox, add them in strip order (the same bits on every rank)
-__global__ void k_p2p_red_finish(P2PArgs a, double* __restrict__ out) {
+__global__ void k_p2p_red_finish(P2PArgs a, double* __restrict__ out, DDPost post) {
   const int g0 = a.strip0;
   const unsigned long long seq = *(volatile unsigned long long*)(a.seq + 1) + 1;
   for (int h = threadIdx.x; h < a.G; h += blockDim.x) spin_until(box_u64(a, g0, a.off_redflag) + h, seq);
@@ -360,6 +467,7 @@ __global__ void k_p2p_red_finish(P2PArgs a, double* __restrict__ out) {
     double v = 0.0;
     for (int h = 0; h < a.G; ++h) v += __ldcg(red + h);
     *out = v;
+    dd_post_run(post);
   }
   __syncwarp();
   if (threadIdx.x == 0) *(volatile unsigned long long*)(a.seq + 1) = seq;   // one warp: all have read it
@@ -393,27 +501,12 @@ int p2p_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
   return SCH_OK;
 }
 
-int p2p_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out) {
+int p2p_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out, const DDPost& post) {
   const P2PArgs a = p2p_args(dd);
   k_p2p_red_push<<<dd->S, 256, 0, ctx->stream>>>(part, n, a);
-  k_p2p_red_finish<<<1, 32, 0, ctx->stream>>>(a, out);
+  k_p2p_red_finish<<<1, 32, 0, ctx->stream>>>(a, out, post);
   ctx->launches += 2;
   return SCH_OK;
-}
-
-// ------------------------------------------------------------- CG state
-struct DDState {
-  double* sc;   // scalars: see SC_* below
-  int* flag;    // [S] need_x (X pass) per local strip (all equal)
-  double* beta; // [S] beta per local strip (all equal)
-  int* ctl;     // [0] done, [1] iters, [2] status, [3] current iteration (device-side loop)
-};
-enum { SC_NORMB2 = 0, SC_PAP, SC_RR, SC_TN2, SC_RS, SC_RSNEW, SC_ALPHA, SC_NORMB, SC_TARGET,
-       SC_BEST, SC_RELRES, SC_COUNT };
-
-SCH_DEV bool own_row(long long i, int T, int Lext, int lo, int hi) {
-  const int row = (int)((i / T) % Lext);
-  return row >= lo && row < hi;
 }
 
 // x = x0|0 (all rows), r = p = b (all rows; b halos already exchanged),
@@ -465,19 +558,6 @@ __global__ void k_dd_ctrl_init(DDState st, int S, double tol, int have_x0) {
   st.ctl[3] = 1;
 }
 
-__global__ void k_dd_iter_inc(DDState st) { ++st.ctl[3]; }
-
-// tail of the device-side loop body: iterate while not done (and below the cap)
-__global__ void k_dd_set_continue(DDState st, int maxiter, cudaGraphConditionalHandle h) {
-  cudaGraphSetConditional(h, (st.ctl[0] == 0 && st.ctl[3] <= maxiter) ? 1u : 0u);
-}
-
-__global__ void k_dd_alpha(DDState st) {
-  if (st.ctl[0]) return;
-  const double den = st.sc[SC_PAP];
-  st.sc[SC_ALPHA] = den > 0.0 ? st.sc[SC_RS] / den : 0.0;
-}
-
 // p = r + beta p, x += alpha p on every row; r -= alpha ap and ||r||^2 on own rows
 __global__ void k_dd_update(double2* __restrict__ r, double2* __restrict__ p, double2* __restrict__ x,
                             const double2* __restrict__ ap, DDState st, long long nsites, int T, int Lext,
@@ -504,54 +584,6 @@ __global__ void k_dd_update(double2* __restrict__ r, double2* __restrict__ p, do
   }
   double s = block_sum_rt(acc, slot);
   if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = s;
-}
-
-__global__ void k_dd_check(DDState st, int S) {
-  if (st.ctl[0]) return;
-  const int repl = (st.ctl[3] % kDDReplace) == 0;
-  int need;
-  if (repl) {
-    need = 1;
-  } else {
-    const double rsn = st.sc[SC_RR];
-    st.sc[SC_RSNEW] = rsn;
-    need = sqrt(rsn) <= st.sc[SC_TARGET];
-  }
-  for (int s = 0; s < S; ++s) st.flag[s] = need;
-}
-
-__global__ void k_dd_final(DDState st, int S, int maxiter) {
-  if (st.ctl[0]) return;
-  const int it = st.ctl[3];
-  const int nx = st.flag[0];
-  double rs_new = st.sc[SC_RSNEW];
-  if (nx) {
-    const double tn2 = st.sc[SC_TN2];
-    const double tn = sqrt(tn2);
-    const int repl = (it % kDDReplace) == 0;
-    if (!repl || tn <= st.sc[SC_TARGET]) st.sc[SC_BEST] = tn / st.sc[SC_NORMB];
-    if (tn <= st.sc[SC_TARGET]) {
-      st.ctl[0] = 1;
-      st.ctl[1] = it;
-      st.sc[SC_RELRES] = tn / st.sc[SC_NORMB];
-      for (int s = 0; s < S; ++s) st.flag[s] = 0;
-      return;
-    }
-    rs_new = tn2;
-  }
-  const double rs = st.sc[SC_RS];
-  const double beta = rs > 0.0 ? rs_new / rs : 0.0;
-  for (int s = 0; s < S; ++s) {
-    st.beta[s] = beta;
-    st.flag[s] = 0;
-  }
-  st.sc[SC_RS] = rs_new;
-  if (it >= maxiter) {
-    st.ctl[0] = 1;
-    st.ctl[1] = it;
-    st.ctl[2] = 1;
-    st.sc[SC_RELRES] = fmin(st.sc[SC_BEST], sqrt(rs_new) / st.sc[SC_NORMB]);
-  }
 }
 
 TileShape dd_tiles(int Lext, int T) { return pick_tile(Lext, T, false); }
@@ -839,7 +871,17 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
 
   // One iteration; the iteration number lives on the device (ctl[3]), so the
   // body is the same every time and can be captured.
-  auto iteration = [&](cudaStream_t q) -> int {
+  auto post = [&](int kind, cudaGraphConditionalHandle h = 0) {
+    DDPost p;
+    p.kind = kind;
+    p.st = st;
+    p.S = dd->S;
+    p.maxiter = maxiter;
+    p.set_cond = h != 0;
+    p.h = h;
+    return p;
+  };
+  auto iteration = [&](cudaStream_t q, cudaGraphConditionalHandle h) -> int {
     const cudaStream_t saved = ctx->stream;
     ctx->stream = q;   // dd_exchange / dd_allsum enqueue on ctx->stream
     int e = SCH_OK;
@@ -847,20 +889,17 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
       if ((e = dd_exchange(ctx, dd, (double*)r, 1, 4))) break;
       launch_normal_tile<MODE_P>(sh, tp, q);
       ctx->launches++;
-      if ((e = dd_allsum(ctx, dd, part_a, tpc, st.sc + SC_PAP))) break;
-      k_dd_alpha<<<1, 1, 0, q>>>(st);
+      if ((e = dd_allsum(ctx, dd, part_a, tpc, st.sc + SC_PAP, post(POST_ALPHA)))) break;
       k_dd_update<<<egrid, 256, 0, q>>>(r, p, (double2*)x_ext, ap, st, nsites, dd->T, dd->Lext, lo,
                                         hi, part_b);
-      ctx->launches += 2;
-      if ((e = dd_allsum(ctx, dd, part_b, gx, st.sc + SC_RR))) break;
-      k_dd_check<<<1, 1, 0, q>>>(st, dd->S);
+      ctx->launches++;
+      if ((e = dd_allsum(ctx, dd, part_b, gx, st.sc + SC_RR, post(POST_CHECK)))) break;
       // x halos are current (x is updated on every row), so no exchange here
       launch_normal_tile<MODE_X>(sh, txx, q);
-      ctx->launches += 2;
-      if ((e = dd_allsum(ctx, dd, part_b, tpc, st.sc + SC_TN2))) break;
-      k_dd_final<<<1, 1, 0, q>>>(st, dd->S, maxiter);
-      k_dd_iter_inc<<<1, 1, 0, q>>>(st);
-      ctx->launches += 2;
+      ctx->launches++;
+      // the final control also advances the iteration and, inside the WHILE
+      // graph, sets the loop condition
+      if ((e = dd_allsum(ctx, dd, part_b, tpc, st.sc + SC_TN2, post(POST_FINAL, h)))) break;
       cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) e = sch_fail(ctx, SCH_ERR_CUDA, "dd cg launch: %s", cudaGetErrorString(le));
     } while (0);
@@ -889,8 +928,7 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     SCH_CUDA(ctx, cudaStreamBeginCaptureToGraph(ctx->cap_stream, body, nullptr, nullptr, 0,
                                                 cudaStreamCaptureModeRelaxed));
-    int e = iteration(ctx->cap_stream);
-    k_dd_set_continue<<<1, 1, 0, ctx->cap_stream>>>(st, maxiter, handle);
+    int e = iteration(ctx->cap_stream, handle);
     cudaGraph_t captured;
     cudaError_t ce = cudaStreamEndCapture(ctx->cap_stream, &captured);
     if (e || ce != cudaSuccess) {
@@ -909,7 +947,7 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
     while (it <= maxiter) {
       const int n = std::min(chunk, maxiter - it + 1);
       for (int j = 0; j < n; ++j, ++it)
-        if ((rc = iteration(s))) return rc;
+        if ((rc = iteration(s, 0))) return rc;
       SCH_CUDA(ctx, cudaMemcpyAsync(ctx->h_flag, st.ctl, sizeof(int), cudaMemcpyDeviceToHost, s));
       SCH_CUDA(ctx, cudaStreamSynchronize(s));
       if (*ctx->h_flag) break;
