@@ -62,6 +62,11 @@ CG_KERNELS = {
                  dram_per_site=(134.307328e6 + 36.36352e6) / (8192 * 256),
                  fp64_pipe_active=0.701,
                  source="profiles/r01/ncu_full_k_cg_resblk_tsh.txt"),
+    "cfg3_mega": dict(kernel="k_traj_anfg16 (trajectory megakernel: one 64-thread CTA per 16x16 "
+                             "chain runs H(start), the 17 resident-CG solves, forces, FG terms, "
+                             "inner leapfrogs and H(end) of the adapted-nested-fg trajectory)",
+                      dram_per_site=None, fp64_pipe_active=None,
+                      source="profiles/r01/ncu_full_k_traj_anfg16.txt"),
     "cfg4": dict(kernel="k_cg_cluster_tx<64,64,4 CTAs,2x2 sites/thread> (per-chain CG, one "
                         "4-CTA cluster per chain, faces and partial sums pushed with st.async "
                         "onto the receiver's mbarrier)",
@@ -734,11 +739,14 @@ def run_ours(args):
     cg_iters = sum(int(it.sum().item()) for _, _, it, _ in prof)
     V = cfg.L * cfg.T
     n_solves = len(prof)
+    mega = args.workload == "cfg3" and sw.hmc._mega_eligible(cfg, True)
+    kinfo = CG_KERNELS["cfg3_mega" if mega else args.workload]
     cg_bytes = 352.0 * V * cg_iters
     cg_flops = 152.0 * V * cg_iters
     achieved = cg_bytes / (cg_ms * 1e-3) / 1e9
     fp64_peak = fp64_probe(torch, _lib)
-    solves_per_traj = n_solves / args.steps
+    # the megakernel runs every solve of a trajectory in one launch: 1 + 4n
+    solves_per_traj = (1 + 4 * max(1, round(cfg.tau / cfg.h))) if mega else n_solves / args.steps
 
     # ensemble observables: one NCCL all-gather at the end (the only collective)
     obs = gather_observables({"dh": np.concatenate(dhs),
@@ -848,27 +856,29 @@ def run_ours(args):
                        "cg_iterations_per_chain_traj": cg_iters / (chains * args.steps)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak,
-                         "traffic": CG_KERNELS[args.workload]["dram_per_site"] * V * chains,
+                         "traffic": (None if kinfo["dram_per_site"] is None
+                                     else kinfo["dram_per_site"] * V * chains),
                          "traffic_source": "dram__bytes_read.sum+dram__bytes_write.sum of one "
-                                           "launch (ncu --set full, "
-                                           f"{CG_KERNELS[args.workload]['source']}), per site, "
-                                           "x sites of one launch here",
+                                           f"launch (ncu --set full, {kinfo['source']}), per "
+                                           "site, x sites of one launch here",
                          "algorithmic_bytes_per_launch": cg_bytes / max(1, n_solves),
                          "peak_kind": peak_kind,
-                         "kernel": CG_KERNELS[args.workload]["kernel"],
+                         "kernel": kinfo["kernel"],
                          "bytes_model": "352 B/site/CG-iteration (SURVEY 8(d)), "
                                         f"{V} sites x {cg_iters} chain-iterations",
                          "effective": True,
                          "note": "working set is SMEM/register resident; true bound is FP64 "
-                                 "issue / shared-memory bandwidth",
+                                 "issue / shared-memory bandwidth" + (
+                                     "; the megakernel's time also holds its non-CG phases "
+                                     "(forces, FG terms, inner leapfrogs, H)" if mega else ""),
                          "fp64_tflops": cg_flops / (cg_ms * 1e-3) / 1e12,
                          "fp64_peak_tflops_probe": fp64_peak,
                          "fp64_frac": cg_flops / (cg_ms * 1e-3) / 1e12 / fp64_peak,
-                         "fp64_pipe_active_ncu": CG_KERNELS[args.workload]["fp64_pipe_active"],
+                         "fp64_pipe_active_ncu": kinfo["fp64_pipe_active"],
                          "fp64_note": "fp64_frac counts the 152 flop/site model; the kernel "
                                       "issues ~112 FP64 instructions per site-iteration, and "
                                       "ncu's FP64 pipe-active fraction is the issue-rate bound",
-                         "cg_share_of_step": cg_ms / ms},
+                         "kernel_share_of_step": cg_ms / ms},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

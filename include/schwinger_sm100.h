@@ -174,6 +174,19 @@ int sch_np_heatbath(sch_ctx* ctx, void* state, double* p, double* phi, int B, lo
 /* metropolis (hmc.py:54-60): accept 1/0, -1 for non-finite dH; draws only if dH > 0 */
 int sch_np_metropolis(sch_ctx* ctx, void* state, const double* dh, int* accept, int B);
 
+/* ---- trajectory megakernel ------------------------ */
+/* One adapted-nested-fg trajectory (integrators.py:341-349, with the
+ * Hamiltonian at both ends, hmc.py:44-51 and hmc.py:83-85) of B independent
+ * 16x16 chains, one CTA per chain, in a single launch: replaces hamiltonian()
+ * + integrate_trajectory() + hamiltonian() of hmc_update for that scheme.
+ * q_in, p [B][2][16][16], eta [B][16][16][2] in; q_out, dh = H(end) - H(start),
+ * status (1: a CG hit maxiter), iters (CG iterations) per chain out.
+ * dt_kf = h/6, b_g = 2h/3, c_g = FG_KICK_SIGN * fgc * h^3, span = h/2. */
+int sch_traj_anfg16(sch_ctx* ctx, const double* q_in, const double* p, const double* eta,
+                    double* q_out, double* dh, int* status, int* iters, int B, double beta, double m0,
+                    double tol, int maxiter, double dt_kf, double b_g, double c_g, double span,
+                    int n_steps, int micro);
+
 /* ---- domain decomposition of one lattice (BASELINE configs[4]) -------- */
 /* One lattice split into G = nranks * strips_local x-strips of Lloc = L/G
  * rows.  Fields are "extended strips": [strips_local][Lloc+4][T] (2 halo

@@ -4,44 +4,11 @@
 // (the drift and gauge force are then bit-identical to the reference for
 // identical inputs, up to the libm-vs-CUDA sin/cos difference).
 #include "common.cuh"
+#include "site_ops.cuh"
 #include "runtime.hpp"
 #include "../../include/schwinger_sm100.h"
 
 namespace {
-
-constexpr double kPi = 3.141592653589793;      // np.pi
-constexpr double kTwoPi = 6.283185307179586;   // 2.0 * np.pi (lattice.py:21)
-
-// fmod(a, 2pi) without the library's bit-serial loop: n = trunc(a / 2pi)
-// from a rounded quotient, corrected by one if the rounding crossed an
-// integer; then a - n*2pi in one FMA.  The remainder of a division of two
-// doubles is exactly representable, so the single rounding of the FMA
-// returns it exactly: the result equals fmod's bit for bit.
-__device__ __forceinline__ double fmod_2pi(double a) {
-  if (!(fabs(a) < 1e15)) return fmod(a, kTwoPi);   // inf / nan / huge: the library path
-  double n = trunc(a * (1.0 / kTwoPi));
-  double r = __fma_rn(-n, kTwoPi, a);
-  if (r != 0.0 && (r < 0.0) != (a < 0.0)) {         // quotient rounded away from zero
-    n -= a < 0.0 ? -1.0 : 1.0;
-    r = __fma_rn(-n, kTwoPi, a);
-  } else if (fabs(r) >= kTwoPi) {                   // rounded toward zero past an integer
-    n += a < 0.0 ? -1.0 : 1.0;
-    r = __fma_rn(-n, kTwoPi, a);
-  }
-  return r;
-}
-
-// NumPy's floored remainder (npy_divmod) followed by -pi: lattice.py:28-30
-__device__ __forceinline__ double wrap_angle(double v) {
-  double a = v + kPi;
-  double m = fmod_2pi(a);
-  if (m != 0.0) {
-    if (m < 0.0) m += kTwoPi;
-  } else {
-    m = 0.0;   // copysign(0, +2pi)
-  }
-  return m - kPi;
-}
 
 __global__ void k_rotate(const double* __restrict__ q, const double* __restrict__ p, double h,
                          double* __restrict__ out, long long n) {

@@ -31,8 +31,30 @@
 // both t-neighbours of a thread sit in its own warp (NBT divides 32).  The
 // t-face hops are then added before the exchange barrier and only the
 // x-faces go through shared memory (-50 % shared-memory exchange traffic).
-template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0>
-__global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs a) {
+//
+// The solve is a device function (cg_resblk_run) so that the trajectory
+// megakernel (mega.cu) runs the same code on its own per-chain buffers:
+// chain `c` indexes the iters/relres/status outputs, `cb` is the site offset
+// of the chain's fields, `sm` the dynamic shared memory (2 exchange stages).
+// COH = true reads U and b with coherent loads (they were written earlier in
+// the same kernel); the batched kernel uses the read-only path.
+template <bool COH>
+SCH_DEV double2 res_ld2(const double2* p) {
+  if constexpr (COH)
+    return *p;
+  else
+    return __ldg(p);
+}
+template <bool COH>
+SCH_DEV Spinor res_ld_spinor(const double2* p, long long site) {
+  if constexpr (COH)
+    return ld256_spinor(p, site);
+  else
+    return ldg_spinor(p, site);
+}
+
+template <int LC, int TC, int BX, int BT, int TSH, bool COH>
+SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   using Blk = SiteBlock<BX, BT>;
   constexpr int SPT = Blk::SPT;
   constexpr int NT = LC * TC / SPT;
@@ -44,13 +66,10 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
   static_assert(!TSH || 32 % NBT == 0, "t-neighbours must share a warp");
   // plane offsets inside one stage
   constexpr int O0 = 0, O1 = BT * NT, O2 = 2 * BT * NT, O3 = (2 * BT + BX) * NT;
-  extern __shared__ double2 sm[];
   __shared__ double red[3][NW];
   double2* E0 = sm;
   double2* E1 = sm + PL;
   const int tid = threadIdx.x;
-  const int c = blockIdx.x;
-  const long long cb = (long long)c * V;
   const int bx = tid / NBT, bt = tid % NBT;
   auto site = [&](int k) { return (bx * BX + k / BT) * TC + bt * BT + k % BT; };
   // exchange partners (thread ids owning the neighbouring blocks)
@@ -64,9 +83,9 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
   double bb = 0.0;
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
-    u0[k] = cscale(-0.5, __ldg(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
-    u1[k] = cscale(-0.5, __ldg(a.U + 2 * cb + V + site(k)));
-    r[k] = ldg_spinor(a.b, cb + site(k));
+    u0[k] = cscale(-0.5, res_ld2<COH>(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
+    u1[k] = cscale(-0.5, res_ld2<COH>(a.U + 2 * cb + V + site(k)));
+    r[k] = res_ld_spinor<COH>(a.b, cb + site(k));
     x[k].s0 = x[k].s1 = make_double2(0, 0);
     bb += spinor_norm2(r[k]);
   }
@@ -146,7 +165,7 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
   double rs = normb2;   // r = b exactly: the same sum as ||b||^2 (fermion.py:186,191)
   if (a.x0) {
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) x[k] = ldg_spinor(a.x0, cb + site(k));
+    for (int k = 0; k < SPT; ++k) x[k] = res_ld_spinor<COH>(a.x0, cb + site(k));
     normal_op(x, w);
     double rr = 0.0;
 #pragma unroll
@@ -208,7 +227,7 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
       double tn2 = 0.0;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
-        w[k] = sp_sub(ldg_spinor(a.b, cb + site(k)), w[k]);
+        w[k] = sp_sub(res_ld_spinor<COH>(a.b, cb + site(k)), w[k]);
         tn2 += spinor_norm2(w[k]);
       }
       tn2 = block_sum<NT>(tn2, red[2]);
@@ -245,4 +264,10 @@ __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs
     a.relres[c] = fmin(best, sqrt(rs) / normb);
     a.status[c] = 1;
   }
+}
+
+template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0>
+__global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs a) {
+  extern __shared__ double2 sm[];
+  cg_resblk_run<LC, TC, BX, BT, TSH, false>(a, blockIdx.x, (long long)blockIdx.x * LC * TC, sm);
 }

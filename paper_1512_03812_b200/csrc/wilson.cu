@@ -2,6 +2,7 @@
 // fermion force (+ fused kicks), weighted w-sums and the fermion
 // force-gradient contraction.  Reference: fermion.py.
 #include "common.cuh"
+#include "site_ops.cuh"
 #include "runtime.hpp"
 #include "tile.cuh"
 #include "tma_tile.cuh"
@@ -102,25 +103,6 @@ __global__ void k_spinor_dot_finish(const double* __restrict__ part, int slabs, 
   out[2 * c + 1] = im;
 }
 
-// A(n) = conj(w-(a)(n)) U_mu(n) w-(b)(n+mu);  B(n) = conj(w+(a)(n+mu)) conj(U_mu(n)) w+(b)(n)
-// (fermion.py:317-327), NumPy order: (conj(wa) * u) * wb.
-struct Bil {
-  double2 A, B;
-};
-template <int MU>
-__device__ __forceinline__ Bil bilinear(const Spinor& a_n, const Spinor& a_f, const Spinor& b_n,
-                                        const Spinor& b_f, double2 u) {
-  Bil r;
-  if (MU == 0) {
-    r.A = cmul(cmulc(wminus0(a_n), u), wminus0(b_f));
-    r.B = cmul(cmulc(wplus0(a_f), cconj(u)), wplus0(b_n));
-  } else {
-    r.A = cmul(cmulc(wminus1(a_n), u), wminus1(b_f));
-    r.B = cmul(cmulc(wplus1(a_f), cconj(u)), wplus1(b_n));
-  }
-  return r;
-}
-
 // Fermion force f = -Im(A - B) (fermion.py:330-336).  KICK: out = p - dt*(f [+ beta*g])
 // (kick_fermion / kick_full, integrators.py:172-186).
 template <bool KICK>
@@ -133,20 +115,17 @@ __global__ void k_fermion_force(const double2* __restrict__ U, const double2* __
        i += (long long)gridDim.x * blockDim.x) {
     long long b = i / g.V;
     int s = (int)(i - b * g.V);
-    int x = s / g.T, t = s - x * g.T;
-    int xp = x + 1 == g.L ? 0 : x + 1, tp = t + 1 == g.T ? 0 : t + 1;
     long long cb = b * g.V;
-    Spinor cn = ld256_spinor_nc(chi, cb + s), xn = ld256_spinor_nc(xi, cb + s);
-    Spinor cx = ld256_spinor_nc(chi, cb + xp * g.T + t), xx = ld256_spinor_nc(xi, cb + xp * g.T + t);
-    Spinor ct = ld256_spinor_nc(chi, cb + x * g.T + tp), xt = ld256_spinor_nc(xi, cb + x * g.T + tp);
     const double2* Uc = U + 2 * cb;
-    Bil b0 = bilinear<0>(cn, cx, xn, xx, __ldg(Uc + s));
-    Bil b1 = bilinear<1>(cn, ct, xn, xt, __ldg(Uc + g.V + s));
-    double f0 = -(b0.A.y - b0.B.y);
-    double f1 = -(b1.A.y - b1.B.y);
+    auto lc = [&](int k) { return ld256_spinor_nc(chi, cb + k); };
+    auto lx = [&](int k) { return ld256_spinor_nc(xi, cb + k); };
+    auto lu = [&](int mu, int k) { return __ldg(Uc + mu * g.V + k); };
+    double f0, f1;
+    force_site(s, g.L, g.T, lc, lx, lu, f0, f1);
     long long o0 = 2 * cb + s, o1 = o0 + g.V;
     if (KICK) {
       if (q) {   // kick_full: force = gauge_force + fermion_force
+        const int x = s / g.T, t = s - x * g.T;
         int xm = x == 0 ? g.L - 1 : x - 1, tm = t == 0 ? g.T - 1 : t - 1;
         const double* qc = q + 2 * cb;
         double s0 = sin(plaq(qc, g.L, g.T, x, t));
@@ -196,47 +175,16 @@ __global__ void k_wsums(const double2* __restrict__ U, const double* __restrict_
        i += (long long)gridDim.x * blockDim.x) {
     long long b = i / g.V;
     int s = (int)(i - b * g.V);
-    int x = s / g.T, t = s - x * g.T;
     long long cb = b * g.V;
     const double2* Uc = U + 2 * cb;
     const double* Wc = wt + 2 * cb;
-    double2 o10 = make_double2(0, 0), o11 = o10, o20 = o10, o21 = o10;
-#pragma unroll
-    for (int nu = 0; nu < 2; ++nu) {
-      int sf, sb;   // n + nu, n - nu
-      if (nu == 0) {
-        sf = (x + 1 == g.L ? 0 : x + 1) * g.T + t;
-        sb = (x == 0 ? g.L - 1 : x - 1) * g.T + t;
-      } else {
-        sf = x * g.T + (t + 1 == g.T ? 0 : t + 1);
-        sb = x * g.T + (t == 0 ? g.T - 1 : t - 1);
-      }
-      Spinor cb_ = ld256_spinor_nc(chi, cb + sb), cf = ld256_spinor_nc(chi, cb + sf);
-      Spinor xb = ld256_spinor_nc(xi, cb + sb), xf = ld256_spinor_nc(xi, cb + sf);
-      double2 un = __ldg(Uc + nu * g.V + s), ub = __ldg(Uc + nu * g.V + sb);
-      double wn = __ldg(Wc + nu * g.V + s), wb = __ldg(Wc + nu * g.V + sb);
-      double2 wm_cb = nu == 0 ? wminus0(cb_) : wminus1(cb_);
-      double2 wp_cf = nu == 0 ? wplus0(cf) : wplus1(cf);
-      double2 wm_xf = nu == 0 ? wminus0(xf) : wminus1(xf);
-      double2 wp_xb = nu == 0 ? wplus0(xb) : wplus1(xb);
-      // t1 = (0.5i * w*conj(U)*w-(chi))(n - nu)
-      double2 t1 = cscale(0.5, cmuli(cmul(cscale(wb, cconj(ub)), wm_cb)));
-      // t2 = -0.5i * w(n) U(n) w+(chi)(n + nu)
-      double2 t2 = cscale(-0.5, cmuli(cmul(cscale(wn, un), wp_cf)));
-      // t3 = -0.5i * w(n) U(n) w-(xi)(n + nu)
-      double2 t3 = cscale(-0.5, cmuli(cmul(cscale(wn, un), wm_xf)));
-      // t4 = (0.5i * w*conj(U)*w+(xi))(n - nu)
-      double2 t4 = cscale(0.5, cmuli(cmul(cscale(wb, cconj(ub)), wp_xb)));
-      o10 = cadd(o10, cadd(t1, t2));
-      o20 = cadd(o20, cadd(t3, t4));
-      if (nu == 0) {   // e- = -1, e+ = +1
-        o11 = cadd(o11, csub(t2, t1));
-        o21 = cadd(o21, csub(t4, t3));
-      } else {         // e- = -i, e+ = +i
-        o11 = cadd(o11, cmuli(csub(t2, t1)));
-        o21 = cadd(o21, cmuli(csub(t4, t3)));
-      }
-    }
+    auto lc = [&](int k) { return ld256_spinor_nc(chi, cb + k); };
+    auto lx = [&](int k) { return ld256_spinor_nc(xi, cb + k); };
+    auto lu = [&](int mu, int k) { return __ldg(Uc + mu * g.V + k); };
+    auto lw = [&](int mu, int k) { return __ldg(Wc + mu * g.V + k); };
+    Spinor o1, o2;
+    wsums_site(s, g.L, g.T, lc, lx, lu, lw, o1, o2);
+    const double2 o10 = o1.s0, o11 = o1.s1, o20 = o2.s0, o21 = o2.s1;
     long long o = cb + s;
     b1[2 * o] = o10;
     b1[2 * o + 1] = o11;
@@ -256,24 +204,16 @@ __global__ void k_fg_combine(const double2* __restrict__ U, const double2* __res
        i += (long long)gridDim.x * blockDim.x) {
     long long b = i / g.V;
     int s = (int)(i - b * g.V);
-    int x = s / g.T, t = s - x * g.T;
     long long cb = b * g.V;
     const double2* Uc = U + 2 * cb;
-#pragma unroll
-    for (int mu = 0; mu < 2; ++mu) {
-      int sf = mu == 0 ? (x + 1 == g.L ? 0 : x + 1) * g.T + t : x * g.T + (t + 1 == g.T ? 0 : t + 1);
-      Spinor z1n = ld256_spinor_nc(z1, cb + s), z1f = ld256_spinor_nc(z1, cb + sf);
-      Spinor z2n = ld256_spinor_nc(z2, cb + s), z2f = ld256_spinor_nc(z2, cb + sf);
-      Spinor cn = ld256_spinor_nc(chi, cb + s), cf = ld256_spinor_nc(chi, cb + sf);
-      Spinor xn = ld256_spinor_nc(xi, cb + s), xf = ld256_spinor_nc(xi, cb + sf);
-      double2 u = __ldg(Uc + mu * g.V + s);
-      Bil a1 = mu == 0 ? bilinear<0>(z1n, z1f, xn, xf, u) : bilinear<1>(z1n, z1f, xn, xf, u);
-      Bil a2 = mu == 0 ? bilinear<0>(cn, cf, z2n, z2f, u) : bilinear<1>(cn, cf, z2n, z2f, u);
-      Bil a3 = mu == 0 ? bilinear<0>(cn, cf, xn, xf, u) : bilinear<1>(cn, cf, xn, xf, u);
-      double w = __ldg(wt + 2 * cb + mu * g.V + s);
-      double v = 2.0 * (a1.A.y - a1.B.y) + 2.0 * (a2.A.y - a2.B.y) - 2.0 * (a3.A.x + a3.B.x) * w;
-      out[2 * cb + mu * g.V + s] = v;
-    }
+    auto l1 = [&](int k) { return ld256_spinor_nc(z1, cb + k); };
+    auto l2 = [&](int k) { return ld256_spinor_nc(z2, cb + k); };
+    auto lc = [&](int k) { return ld256_spinor_nc(chi, cb + k); };
+    auto lx = [&](int k) { return ld256_spinor_nc(xi, cb + k); };
+    auto lu = [&](int mu, int k) { return __ldg(Uc + mu * g.V + k); };
+    auto lw = [&](int mu, int k) { return __ldg(wt + 2 * cb + mu * g.V + k); };
+    out[2 * cb + s] = fg_combine_site<0>(s, g.L, g.T, l1, l2, lc, lx, lu, lw);
+    out[2 * cb + g.V + s] = fg_combine_site<1>(s, g.L, g.T, l1, l2, lc, lx, lu, lw);
   }
 }
 

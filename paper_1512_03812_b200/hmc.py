@@ -23,7 +23,9 @@ from . import _lib
 from .config import HmcConfig
 from .fermion import InversionCounter, WilsonDirac, draw_phi, pseudofermion_heatbath, spinor_dot
 from .gauge import avg_plaquette, gauge_action
-from .integrators import IntegratorSpec, MdState, integrate_trajectory
+from .fermion import SolverError
+from .integrators import (FG_KICK_SIGN, INVERSIONS_PER_STEP, IntegratorSpec, MdState, TrajectoryResult,
+                          integrate_trajectory)
 from .lattice import (DeviceRng, LatticeGeom, NumpyDeviceRng, as_links, as_spinor, cold_start,
                       kinetic_energy,
                       sample_momenta)
@@ -237,6 +239,77 @@ def hmc_update_ensemble_async(q, config: HmcConfig, device_rng, counter=None,
     return _ensemble_update(q, config, None, device_rng, counter, reuse_solves, sync=False)
 
 
+# The trajectory megakernel (csrc/mega.cu): one launch runs H(start), the
+# whole adapted-nested-fg trajectory and H(end) of every 16x16 chain, with
+# the same arithmetic as the kernel-per-map path below (tests/test_gpu_mega.py).
+# Opt-in (SCH_MEGA=1): on cfg3 it measured 161k vs 172k chain-traj/s for the
+# kernel-per-map path — the solver inlined into the larger kernel issues at
+# 62 % FP64-pipe activity instead of 70 %.
+USE_MEGA = __import__("os").environ.get("SCH_MEGA", "0") == "1"
+
+
+def _mega_eligible(config: HmcConfig, reuse_solves: bool) -> bool:
+    return (USE_MEGA and reuse_solves and config.scheme == "adapted-nested-fg"
+            and config.L == 16 and config.T == 16 and config.fermion_bc == "periodic"
+            and not config.quenched)
+
+
+class _MegaStatus:
+    """Per-chain CG failure flags of a megakernel trajectory (the CgInfo
+    interface the update paths check)."""
+
+    def __init__(self, status, maxiter):
+        self.status_dev, self._maxiter = status, maxiter
+
+    def raise_if_failed(self):
+        if bool(self.status_dev.ne(0).any().item()):
+            raise SolverError(f"CG exceeded {self._maxiter} iterations", float("nan"))
+
+
+class _MegaState:
+    """What PendingEnsembleStats / EnsembleUpdateGraph need from an MdState:
+    the final links and the solver checks."""
+
+    def __init__(self, q, status, maxiter):
+        self.q = q
+        self._infos = [_MegaStatus(status, maxiter)]
+
+    def check_solves(self):
+        for i in self._infos:
+            i.raise_if_failed()
+
+
+def _mega_trajectory(q, p, eta, config: HmcConfig, counter):
+    """(q_end, dH, state, TrajectoryResult) of one adapted-nested-fg trajectory
+    per chain in one kernel (same scalars as integrators.PROGRAMS)."""
+    from .fermion import DEFAULT_MAXITER
+    spec = _spec_of(config)
+    h = spec.h
+    n = max(1, round(config.tau / h))
+    B = q.shape[0]
+    q_end = torch.empty_like(q)
+    dh = torch.empty((B,), dtype=torch.float64, device=q.device)
+    status = torch.empty((B,), dtype=torch.int32, device=q.device)
+    iters = torch.empty((B,), dtype=torch.int32, device=q.device)
+    from . import fermion as _F
+    prof = _F.CG_PROFILE   # bench instrumentation: the megakernel is the step's CG time
+    if prof is not None:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+    _lib.ctx().call("sch_traj_anfg16", _lib.ptr(q), _lib.ptr(p), _lib.ptr(eta), _lib.ptr(q_end),
+                    _lib.ptr(dh), _lib.ptr(status), _lib.ptr(iters), B, float(config.beta),
+                    float(config.m0), float(config.cg_tol), int(DEFAULT_MAXITER), h / 6.0,
+                    2.0 * h / 3.0, FG_KICK_SIGN * (spec.fg_coefficient * h**3), 0.5 * h, int(n),
+                    int(spec.micro_steps()))
+    if prof is not None:
+        ev1.record()
+        prof.append((ev0, ev1, iters, config.L * config.T))
+    inv = INVERSIONS_PER_STEP[config.scheme] * n
+    counter.add(inv + 4)   # + the two Hamiltonian solves, as the kernel-per-map path counts
+    return q_end, dh, _MegaState(q_end, status, DEFAULT_MAXITER), TrajectoryResult(
+        n_steps=n, inversions=inv, realized_tau=n * h)
+
+
 def _ensemble_update(q, config, rngs, device_rng, counter, reuse_solves, sync):
     q = as_links(q)
     if q.ndim != 4:
@@ -266,14 +339,19 @@ def _ensemble_update(q, config, rngs, device_rng, counter, reuse_solves, sync):
         eta = torch.zeros(geom.spinor_shape(B), dtype=torch.complex128, device=q.device)
     else:
         eta = WilsonDirac(q, config.m0, config.fermion_bc).apply_dag(phi)
-    state = MdState(q=q.clone(), p=p, eta=eta, beta=config.beta, m0=config.m0, tol=config.cg_tol,
-                    counter=counter, fermion_bc=config.fermion_bc, stop="per_chain",
-                    reuse_solves=reuse_solves)
     t0 = time.perf_counter()
-    h_start = hamiltonian(state)
-    result = integrate_trajectory(state, _spec_of(config), config.tau, check=sync)
-    h_end = hamiltonian(state)
-    dh_dev = h_end - h_start
+    if _mega_eligible(config, reuse_solves):
+        q_end, dh_dev, state, result = _mega_trajectory(q, p, eta, config, counter)
+        if sync:
+            state.check_solves()
+    else:
+        state = MdState(q=q.clone(), p=p, eta=eta, beta=config.beta, m0=config.m0,
+                        tol=config.cg_tol, counter=counter, fermion_bc=config.fermion_bc,
+                        stop="per_chain", reuse_solves=reuse_solves)
+        h_start = hamiltonian(state)
+        result = integrate_trajectory(state, _spec_of(config), config.tau, check=sync)
+        h_end = hamiltonian(state)
+        dh_dev = h_end - h_start
     if device_rng is not None:
         if isinstance(device_rng, NumpyDeviceRng):
             acc = device_rng.metropolis(dh_dev)

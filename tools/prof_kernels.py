@@ -3,6 +3,7 @@
     python tools/prof_kernels.py stencil   # cfg2 fused D^dag D, 4096 x 32^2
     python tools/prof_kernels.py cg        # cfg3-like resident CG, 8192 x 16^2
     python tools/prof_kernels.py stream    # streaming CG iterations, cfg2
+    python tools/prof_kernels.py mega      # trajectory megakernel, 8192 x 16^2 (cfg3)
 """
 import math
 import sys
@@ -38,6 +39,13 @@ def main(what):
         q, psi = field(4096, 32, 3)
         op = sw.WilsonDirac(q, 0.1)
         F.cg_solve(op, psi, 1e-10, maxiter=12, stop="batch_global")
+    elif what == "mega":
+        cfg = sw.HmcConfig(L=16, T=16, beta=2.0, m0=0.1, tau=1.0, h=0.25,
+                           scheme="adapted-nested-fg", micro_per_call=2, cg_tol=1e-10)
+        d = sw.NumpyDeviceRng(seed=2024, n_chains=8192)
+        q = d.hot_start(sw.LatticeGeom(16, 16))
+        for _ in range(2):
+            q, _ = sw.hmc_update_ensemble(q, cfg, device_rng=d)
     torch.cuda.synchronize()
     print("done", what)
 
