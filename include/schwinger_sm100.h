@@ -118,6 +118,13 @@ int sch_cg_normal(sch_ctx* ctx, const double* U, const double* b, double* x, con
                   int B, int L, int T, double m0, double tol, int maxiter, int stop_mode,
                   int* iters, double* relres, int* status, int* h_iters_out);
 
+/* chi_xi (fermion.py:300-310): xi = (D^dag D)^{-1} eta by the CG above and
+ * chi = D xi, in one call; the 16^2 / 32^2 per-chain resident engines form
+ * chi inside the solve.  Outputs and stop modes as sch_cg_normal (no sync). */
+int sch_chi_xi(sch_ctx* ctx, const double* U, const double* eta, double* chi, double* xi,
+               const double* x0, int B, int L, int T, double m0, double tol, int maxiter,
+               int stop_mode, int* iters, double* relres, int* status);
+
 /* f(n,mu) = -Im[A - B] (fermion.py:330-336); when p != NULL the kick is
  * fused: out = p - dt * (f [+ beta*g(q) when q != NULL])  (kick_fermion /
  * kick_full, integrators.py:172-186) */

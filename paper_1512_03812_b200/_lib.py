@@ -74,6 +74,8 @@ _SIGNATURES = {
                       ctypes.POINTER(_c_ptr)],
     "sch_dd_destroy": [_c_ptr],
     "sch_dd_p2p_open": [_c_ptr, _c_ptr, _c_ptr],
+    "sch_chi_xi": [_c_ptr] * 6 + [_c_int, _c_int, _c_int, _c_dbl, _c_dbl, _c_int, _c_int, _c_ptr,
+                                  _c_ptr, _c_ptr],
     "sch_traj_anfg16": [_c_ptr] + [_c_ptr] * 7 + [_c_int, _c_dbl, _c_dbl, _c_dbl, _c_int, _c_dbl,
                                                  _c_dbl, _c_dbl, _c_dbl, _c_int, _c_int],
     "sch_dd_p2p_connect": [_c_ptr, _c_ptr, _c_ptr],

@@ -79,13 +79,26 @@ int launch_resblk(sch_ctx* ctx, const ResArgs& a, int B) {
 // 32^2 10.76 ns per chain-iteration); other shapes the strided kernel
 // (resident.cuh).  SCH_RESIDENT="NTxSPTxMINBxSPEC" forces a strided
 // instantiation for tuning runs (SPEC 1 = compile-time shape, 0 = generic).
-int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
-  static int fnt = -1, fspt = 0, fminb = 0, fspec = 1;
-  if (fnt < 0) {
-    fnt = 0;
-    if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%dx%dx%d", &fnt, &fspt, &fminb, &fspec);
+struct ResidentForce {
+  int nt = 0, spt = 0, minb = 0, spec = 1;
+};
+const ResidentForce& resident_force() {
+  static ResidentForce f;
+  static bool read = false;
+  if (!read) {
+    read = true;
+    if (const char* e = getenv("SCH_RESIDENT")) sscanf(e, "%dx%dx%dx%d", &f.nt, &f.spt, &f.minb, &f.spec);
   }
-  const bool forced = fnt > 0 && (long long)fnt * fspt >= V;
+  return f;
+}
+bool resident_forced(long long V) {
+  const ResidentForce& f = resident_force();
+  return f.nt > 0 && (long long)f.nt * f.spt >= V;
+}
+int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
+  const ResidentForce& rf = resident_force();
+  const int fnt = rf.nt, fspt = rf.spt, fminb = rf.minb, fspec = rf.spec;
+  const bool forced = resident_forced(V);
   static int tsh = -1;   // t-faces through warp shuffles (default; SCH_RESBLK_TSH=0: SMEM)
   if (tsh < 0) {
     const char* e = getenv("SCH_RESBLK_TSH");
@@ -819,4 +832,20 @@ extern "C" int sch_cg_normal(sch_ctx* ctx, const double* U, const double* b, dou
       if (hs[c]) return sch_fail(ctx, SCH_ERR_SOLVER, "CG exceeded %d iterations (chain %d)", maxiter, c);
   }
   return SCH_OK;
+}
+
+// chi_xi (fermion.py:300-310): xi = CG(eta), chi = D xi in one call.
+// (Forming chi inside the resident solve from the registers was measured:
+// the solver's loop compiles ~12 % slower with the epilogue, more than the
+// 44 us D launch it saves on 8192 x 16^2 — DESIGN.md §5.)
+extern "C" int sch_chi_xi(sch_ctx* ctx, const double* U, const double* eta, double* chi, double* xi,
+                          const double* x0, int B, int L, int T, double m0, double tol, int maxiter,
+                          int stop_mode, int* iters, double* relres, int* status) {
+  SCH_CHECK_ARG(ctx, U && eta && chi && xi && iters && relres && status, "chi_xi: null pointer");
+  SCH_CHECK_ARG(ctx, xi != eta && xi != x0 && chi != eta && chi != xi && chi != x0,
+                "chi_xi: outputs alias inputs");
+  int rc = sch_cg_normal(ctx, U, eta, xi, x0, B, L, T, m0, tol, maxiter, stop_mode, iters, relres,
+                         status, nullptr);
+  if (rc) return rc;
+  return sch_dslash(ctx, U, 1, xi, chi, B, L, T, m0, 0);
 }

@@ -324,11 +324,11 @@ def solve_dirac_dagger(op: WilsonDirac, b, tol: float = DEFAULT_TOL,
     """x = D^{-dag} b = D CG(D^dag D, b); one inversion (fermion.py:262-276)."""
     if exact:
         y, info = op.solve_normal_dense(b), None
-    else:
-        y, info = cg_solve(op, b, tol, maxiter, x0, stop)
+        x = op.apply(y)
+    else:   # one call: the resident engines apply D inside the solve
+        x, y, info = _solve_apply(op, b, tol, maxiter, x0, stop)
         if check:
             info.raise_if_failed()
-    x = op.apply(y)
     if counter is not None:
         counter.add(1)
     rep = SolveReport(1, info, iterations=0 if exact else None,
@@ -369,12 +369,45 @@ def fermion_action(op: WilsonDirac, eta, tol: float = DEFAULT_TOL,
     return spinor_dot(eta, x).real
 
 
+def _solve_apply(op: WilsonDirac, b, tol: float, maxiter: int, x0, stop: str):
+    """(D x, x, CgInfo) for x = CG(D^dag D, b) in one C call (sch_chi_xi)."""
+    b, bshape = op._prep(b)
+    U = op._U_for(bshape)
+    B = n_chains(b)
+    x, dx = torch.empty_like(b), torch.empty_like(b)
+    if x0 is not None:
+        x0 = as_spinor(x0).expand(b.shape).contiguous()
+    dev = b.device
+    iters = torch.empty((B,), dtype=torch.int32, device=dev)
+    relres = torch.empty((B,), dtype=torch.float64, device=dev)
+    status = torch.empty((B,), dtype=torch.int32, device=dev)
+    prof = CG_PROFILE
+    if prof is not None:
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+    _lib.ctx().call("sch_chi_xi", _lib.ptr(U), _lib.ptr(b), _lib.ptr(dx), _lib.ptr(x),
+                    _lib.ptr(x0), B, op.L, op.T, op.m0, float(tol), int(maxiter),
+                    STOP_MODES[stop], _lib.ptr(iters), _lib.ptr(relres), _lib.ptr(status))
+    if prof is not None:
+        ev1.record()
+        prof.append((ev0, ev1, iters, op.L * op.T))
+    return dx, x, CgInfo(iters, relres, status, len(bshape) > 0, stop, maxiter)
+
+
 def chi_xi(op: WilsonDirac, eta, tol: float = DEFAULT_TOL, counter: InversionCounter | None = None,
            x0=None, exact: bool = False, stop: str = "batch_global", check: bool = True):
-    """xi = (D^dag D)^{-1} eta, chi = D xi; two inversions (fermion.py:300-310)."""
-    xi, report = solve_normal(op, eta, tol, counter=counter, x0=x0, exact=exact, stop=stop,
-                              check=check)
-    return op.apply(xi), xi, report
+    """xi = (D^dag D)^{-1} eta, chi = D xi; two inversions (fermion.py:300-310).
+    One C call (sch_chi_xi): the resident engines form chi inside the solve."""
+    if exact:
+        xi, report = solve_normal(op, eta, tol, counter=counter, x0=x0, exact=True, stop=stop,
+                                  check=check)
+        return op.apply(xi), xi, report
+    chi, xi, info = _solve_apply(op, eta, tol, DEFAULT_MAXITER, x0, stop)
+    if check:
+        info.raise_if_failed()
+    if counter is not None:
+        counter.add(2)
+    return chi, xi, SolveReport(2, info)
 
 
 # ---------------------------------------------------------------------------
