@@ -573,6 +573,34 @@ def integrator_comparison(torch, sw, F, q0, drng, reps=2, max_tries=8):
     return out
 
 
+def megakernel_leg(torch, sw, q0, drng, cfg, per_gpu_value, reps=3):
+    """the same update through the opt-in trajectory
+    megakernel (csrc/mega.cu, one launch for H, the trajectory and H),
+    timed beside the kernel-per-map path of the bench line."""
+    if not (cfg.scheme == "adapted-nested-fg" and cfg.L == 16 and cfg.T == 16):
+        return None
+    sw.hmc.USE_MEGA = True
+    try:
+        q, _ = sw.hmc_update_ensemble(q0, cfg, device_rng=drng)   # warm-up (workspace, attributes)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        pends = []
+        for _ in range(reps):
+            q, p = sw.hmc_update_ensemble_async(q, cfg, drng)
+            pends.append(p)
+        e1.record()
+        torch.cuda.synchronize()
+        for p in pends:
+            p.resolve()
+    finally:
+        sw.hmc.USE_MEGA = False
+    v = q0.shape[0] / (e0.elapsed_time(e1) / reps * 1e-3)
+    return {"kernel": "k_traj_anfg16", "chain_traj_per_s": v, "vs_kernel_per_map": v / per_gpu_value,
+            "note": "opt-in (SCH_MEGA=1): equal results; its inlined solver loop compiles "
+                    "~10 % longer than k_cg_resblk's (DESIGN.md)"}
+
+
 def _device_for(local, torch):
     """One GPU per rank.  SCH_DIST_BACKEND=gloo (control-flow tests of the
     multi-rank bench on a 1-GPU box) maps ranks onto the visible devices."""
@@ -831,8 +859,11 @@ def run_ours(args):
         graphs = graph_bench(torch, sw)
         if args.workload == "cfg3":
             single = cfg1_bench(torch, sw, cpu1)
+    mega_leg = None
     if rank == 0 and not args.no_compare and S == 1:
         compare = integrator_comparison(torch, sw, F, qs[0], drngs[0])
+        if args.workload == "cfg3" and not sw.hmc.USE_MEGA:
+            mega_leg = megakernel_leg(torch, sw, qs[0], drngs[0], cfg, value / world)
 
     if rank == 0:
         line = {
@@ -887,6 +918,7 @@ def run_ours(args):
             "graph_capture": graphs,
             "integrators": compare,
             "cfg1_single_chain": single,
+            "megakernel": mega_leg,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
