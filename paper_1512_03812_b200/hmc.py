@@ -425,7 +425,7 @@ class EnsembleUpdateGraph:
     def stats(self) -> "EnsembleStats":
         """Host read-back of the last replay (raises like hmc_update_ensemble)."""
         if self._infos:
-            bad = torch.stack([i.status_dev.ne(0).any() for i in self._infos]).any()
+            bad = torch.cat([i.status_dev.reshape(-1) for i in self._infos]).ne(0).any()
             if bool(bad.item()):
                 for i in self._infos:
                     i.raise_if_failed()

@@ -120,7 +120,7 @@ class MdState:
         infos, self._infos = self._infos, []
         if not infos:
             return
-        bad = torch.stack([i.status_dev.ne(0).any() for i in infos]).any()
+        bad = torch.cat([i.status_dev.reshape(-1) for i in infos]).ne(0).any()   # 3 launches
         if bool(bad.item()):
             for i in infos:
                 i.raise_if_failed()
