@@ -99,6 +99,10 @@ def parse():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3",
                     help="cfg3 (default, the bench line) or cfg4 (64^2 light-fermion ensemble)")
     ap.add_argument("--chains", type=int, default=None, help="chains per GPU")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: --chains is the ensemble total, split across the ranks "
+                         "(BASELINE configs[2] reads '8192 chains sharded across 1/2/4/8 GPUs'); "
+                         "default weak scaling: --chains per GPU")
     ap.add_argument("--outer", type=int, default=None, help="outer (fermion) steps per trajectory")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -661,7 +665,8 @@ def run_ours(args):
             stencil["ddagd"]["cpu_baseline"] = cpu_stencil
 
     from paper_1512_03812_b200.ensemble import gather_observables, shard_chains, summarize
-    shard = shard_chains(args.chains * world, world, rank)   # weak scaling: chains per GPU fixed
+    # weak scaling (default): chains per GPU fixed; --strong: the ensemble total fixed
+    shard = shard_chains(args.chains if args.strong else args.chains * world, world, rank)
     chains = shard.count
     cfg = sw.HmcConfig(h=1.0 / args.outer, **CFG3)
     geom = sw.LatticeGeom(cfg.L, cfg.T)
@@ -748,7 +753,7 @@ def run_ours(args):
     if world > 1:
         ms = _max_over_ranks(dist, torch, ms)
     ms_step = ms / args.steps
-    value = chains * world / (ms_step * 1e-3)
+    value = shard.total / (ms_step * 1e-3)   # all ranks' chain-trajectories per step
 
     # dominant kernel: the resident CG (one launch per solve).  Its time is
     # the union of the CG launch intervals (they overlap across streams), so
@@ -849,7 +854,7 @@ def run_ours(args):
         if world > 1:
             ems = _max_over_ranks(dist, torch, ems)
         d2h = sum(b.numel() for b in q_back) * 8 + chains * (8 + 4)
-        e2e = {"value": chains * world / (ems / steps_e2e * 1e-3), "unit": "chain-trajectories/s",
+        e2e = {"value": shard.total / (ems / steps_e2e * 1e-3), "unit": "chain-trajectories/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": ems / steps_e2e}
 
@@ -869,7 +874,8 @@ def run_ours(args):
         line = {
             "metric": "HMC trajectories/s", "value": value, "unit": "chain-trajectories/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+            "vs_baseline": None,
             "dtype": "f64/c128",
             "data": "synthetic: hot start + heatbaths drawn on device from the reference's own "
                     "streams (chain c == make_rng(2024, c), value-identical NumPy Philox/ziggurat)",
@@ -877,7 +883,7 @@ def run_ours(args):
                                    f"beta={cfg.beta}, m0={cfg.m0}, tau={cfg.tau}, adapted-nested-fg "
                                    f"{args.outer}x{cfg.micro_per_call} steps (h={1.0 / args.outer}), "
                                    "CG tol 1e-10 per-chain stop, complex128",
-                       "chains_per_gpu": chains, "global_chains": chains * world,
+                       "chains_per_gpu": chains, "global_chains": shard.total,
                        "parallelism": f"chain-ensemble dp{world}",
                        "l2": "working set > L2 (126 MB); no flush needed",
                        "acceptance": acc_rate, "mean_abs_dh": ens["mean_abs_dh"],
