@@ -52,6 +52,7 @@
 #include "common.cuh"
 #include "runtime.hpp"
 #include "tile.cuh"
+#include "tma_tile.cuh"
 #include "../../include/schwinger_sm100.h"
 
 namespace {
