@@ -57,11 +57,12 @@ FALLBACK_HBM = 6650.0
 #         the true-residual checks; part of it misses L2)
 DRAM_CFG4 = (268.8832e6 + 103.359744e6) / (1024 * 4096)
 CG_KERNELS = {
-    "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread,t-faces by warp shuffle> (per-chain "
-                        "CG, one 64-thread CTA per chain, 4 CTAs/SM)",
-                 dram_per_site=(134.307328e6 + 36.36352e6) / (8192 * 256),
-                 fp64_pipe_active=0.701,
-                 source="profiles/r01/ncu_full_k_cg_resblk_tsh.txt"),
+    "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread,t-faces by warp shuffle,"
+                        "sigma1-diagonal spin basis> (per-chain CG, one 64-thread CTA per chain, "
+                        "4 CTAs/SM)",
+                 dram_per_site=(134.254336e6 + 36.10496e6) / (8192 * 256),
+                 fp64_pipe_active=0.652,
+                 source="profiles/r01/ncu_full_k_cg_resblk_rot.txt"),
     "cfg3_mega": dict(kernel="k_traj_anfg16 (trajectory megakernel: one 64-thread CTA per 16x16 "
                              "chain runs H(start), the 17 resident-CG solves, forces, FG terms, "
                              "inner leapfrogs and H(end) of the adapted-nested-fg trajectory)",
@@ -913,7 +914,7 @@ def run_ours(args):
                          "fp64_frac": cg_flops / (cg_ms * 1e-3) / 1e12 / fp64_peak,
                          "fp64_pipe_active_ncu": kinfo["fp64_pipe_active"],
                          "fp64_note": "fp64_frac counts the 152 flop/site model; the kernel "
-                                      "issues ~112 FP64 instructions per site-iteration, and "
+                                      "issues ~96 FP64 instructions per site-iteration (sigma1-diagonal basis), and "
                                       "ncu's FP64 pipe-active fraction is the issue-rate bound",
                          "kernel_share_of_step": cg_ms / ms},
             "cpu_baseline": cpu,

@@ -58,18 +58,18 @@ int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
-template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0>
+template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0, bool ROT = false>
 int launch_resblk(sch_ctx* ctx, const ResArgs& a, int B) {
   constexpr int NT = LC * TC / (BX * BT);
   const size_t smem = sizeof(double2) * 2 * (2 * BT + 2 * BX) * NT;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB, TSH>,
+    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB, TSH, ROT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  k_cg_resblk<LC, TC, BX, BT, MINB, TSH><<<B, NT, smem, ctx->stream>>>(a);
+  k_cg_resblk<LC, TC, BX, BT, MINB, TSH, ROT><<<B, NT, smem, ctx->stream>>>(a);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
@@ -79,6 +79,18 @@ int launch_resblk(sch_ctx* ctx, const ResArgs& a, int B) {
 // 32^2 10.76 ns per chain-iteration); other shapes the strided kernel
 // (resident.cuh).  SCH_RESIDENT="NTxSPTxMINBxSPEC" forces a strided
 // instantiation for tuning runs (SPEC 1 = compile-time shape, 0 = generic).
+// Resident CG in the sigma1-diagonal spin basis (block_stencil.cuh; default,
+// measured 16^2 2.25 -> 2.07 ns and 32^2 10.48 -> 9.32 ns per chain-iteration);
+// SCH_RESBLK_ROT=0 runs the reference basis.
+bool resblk_rot() {
+  static int rot = -1;
+  if (rot < 0) {
+    const char* e = getenv("SCH_RESBLK_ROT");
+    rot = (e && e[0] == '0') ? 0 : 1;
+  }
+  return rot != 0;
+}
+
 struct ResidentForce {
   int nt = 0, spt = 0, minb = 0, spec = 1;
 };
@@ -104,10 +116,15 @@ int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
     const char* e = getenv("SCH_RESBLK_TSH");
     tsh = (e && e[0] == '0') ? 0 : 1;
   }
-  if (!forced && a.L == 16 && a.T == 16)
+  const bool rot = resblk_rot();
+  if (!forced && a.L == 16 && a.T == 16) {
+    if (rot) return launch_resblk<16, 16, 2, 2, 4, 1, true>(ctx, a, B);
     return tsh ? launch_resblk<16, 16, 2, 2, 4, 1>(ctx, a, B) : launch_resblk<16, 16, 2, 2, 4>(ctx, a, B);
-  if (!forced && a.L == 32 && a.T == 32)
+  }
+  if (!forced && a.L == 32 && a.T == 32) {
+    if (rot) return launch_resblk<32, 32, 2, 2, 1, 1, true>(ctx, a, B);
     return tsh ? launch_resblk<32, 32, 2, 2, 1, 1>(ctx, a, B) : launch_resblk<32, 32, 2, 2, 1>(ctx, a, B);
+  }
   int nt, spt, minb;
   bool spec = true;
   if (forced) {
@@ -134,11 +151,11 @@ int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
 }
 
 // Cluster-resident CG (resident_cluster.cuh): CS CTAs per chain.
-template <int LC, int TC, int CS, int BX, int BT, int MINB>
+template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = true>
 int launch_cluster(sch_ctx* ctx, const ResArgs& a, int B) {
   constexpr int NT = LC * TC / (CS * BX * BT);
   const size_t smem = sizeof(double2) * 2 * (2 * BT + 2 * BX) * NT;
-  auto kern = k_cg_cluster<LC, TC, CS, BX, BT, MINB>;
+  auto kern = k_cg_cluster<LC, TC, CS, BX, BT, MINB, ROT>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -152,13 +169,13 @@ int launch_cluster(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
-template <int LC, int TC, int CS, int BX, int BT, int MINB>
+template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = true>
 int launch_cluster_tx(sch_ctx* ctx, const ResArgs& a, int B) {
   constexpr int NT = LC * TC / (CS * BX * BT);
   constexpr int PL = (2 * BT + 2 * BX) * NT;
   constexpr int FACE = BT * (TC / BT);
   const size_t smem = sizeof(double2) * (2 * PL + 8 * FACE);
-  auto kern = k_cg_cluster_tx<LC, TC, CS, BX, BT, MINB>;
+  auto kern = k_cg_cluster_tx<LC, TC, CS, BX, BT, MINB, ROT>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -187,7 +204,9 @@ int cluster_dispatch(sch_ctx* ctx, const ResArgs& a, int B) {
     sync_mode = (e && e[0] == '1') ? 1 : 0;
   }
   if (a.L == 64 && a.T == 64 && !sync_mode) {
-    if (cs == 4) return launch_cluster_tx<64, 64, 4, 2, 2, 1>(ctx, a, B);
+    if (cs == 4)
+      return resblk_rot() ? launch_cluster_tx<64, 64, 4, 2, 2, 1>(ctx, a, B)
+                          : launch_cluster_tx<64, 64, 4, 2, 2, 1, false>(ctx, a, B);
     if (cs == 8) return launch_cluster_tx<64, 64, 8, 2, 2, 2>(ctx, a, B);
   }
   if (a.L == 64 && a.T == 64 && cs == 4) return launch_cluster<64, 64, 4, 2, 2, 1>(ctx, a, B);

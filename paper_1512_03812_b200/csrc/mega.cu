@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(MNT, 4) k_traj_anfg16(MegaArgs a) {
     r.diag = a.diag;
     r.tol = a.tol;
     r.maxiter = a.maxiter;
-    cg_resblk_run<ML, MT, 2, 2, 1, true>(r, c, 0, cgsm);
+    cg_resblk_run<ML, MT, 2, 2, 1, true, true>(r, c, 0, cgsm);
     __syncthreads();
     if (tid == 0) {
       sh_it += a.cg_it[c];

@@ -46,7 +46,7 @@ SCH_DEV double2 ld_dsmem(uint32_t addr) {
   return v;
 }
 
-template <int LC, int TC, int CS, int BX, int BT, int MINB>
+template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = false>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX * BT), MINB)
     k_cg_cluster(ResArgs a) {
   namespace cgx = cooperative_groups;
@@ -108,9 +108,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   double bb = 0.0;
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
-    u0[k] = cscale(-0.5, __ldg(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
+    u0[k] = cscale(ROT ? -1.0 : -0.5, __ldg(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
     u1[k] = cscale(-0.5, __ldg(a.U + 2 * cb + V + site(k)));
-    r[k] = ldg_spinor(a.b, cb + site(k));
+    r[k] = rot_in<ROT>(ldg_spinor(a.b, cb + site(k)));
     x[k].s0 = x[k].s1 = make_double2(0, 0);
     bb += spinor_norm2(r[k]);
   }
@@ -121,7 +121,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   const double target = a.tol * normb;
   if (normb == 0.0) {   // fermion.py:181-182, per chain
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), x[k]);
+    for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(x[k]));
     if (tid == 0 && rank == 0) {
       a.iters[c] = 0;
       a.relres[c] = 0.0;
@@ -133,7 +133,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   const double t2 = target * target;
   const double t2lo = t2 * (1.0 - 4e-15), t2hi = t2 * (1.0 + 4e-15);
 
-  using Blk = SiteBlock<BX, BT>;
+  using Blk = std::conditional_t<ROT, SiteBlockRot<BX, BT>, SiteBlock<BX, BT>>;   // ROT: block_stencil.cuh
   auto produce = [&](auto dag, double2* E, const Spinor* v) {
     Blk::template produce<decltype(dag)::value>(u0, u1, v, [&](int plane, int idx, double2 val) {
       constexpr int off[4] = {O0, O1, O2, O3};
@@ -182,7 +182,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   double rs = normb2;   // r = b exactly: the same sum as ||b||^2 (fermion.py:186,191)
   if (a.x0) {
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) x[k] = ldg_spinor(a.x0, cb + site(k));
+    for (int k = 0; k < SPT; ++k) x[k] = rot_in<ROT>(ldg_spinor(a.x0, cb + site(k)));
     normal_op(x, w);
     double rr = 0.0;
 #pragma unroll
@@ -254,7 +254,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
       double tn2 = 0.0;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
-        w[k] = sp_sub(ldg_spinor(a.b, cb + site(k)), w[k]);
+        w[k] = sp_sub(rot_in<ROT>(ldg_spinor(a.b, cb + site(k))), w[k]);
         tn2 += spinor_norm2(w[k]);
       }
       publish(tn2, 2);
@@ -282,7 +282,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
     inv_rs = __drcp_rn(rs);
   }
 #pragma unroll
-  for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), x[k]);
+  for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(x[k]));
   if (tid == 0 && rank == 0) {
     a.iters[c] = status == 0 ? it : a.maxiter;
     a.relres[c] = status == 0 ? relres : fmin(best, sqrt(rs) / normb);
@@ -328,7 +328,7 @@ SCH_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
-template <int LC, int TC, int CS, int BX, int BT, int MINB>
+template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = false>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX * BT), MINB)
     k_cg_cluster_tx(ResArgs a) {
   namespace cgx = cooperative_groups;
@@ -411,9 +411,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   double bb = 0.0;
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
-    u0[k] = cscale(-0.5, __ldg(a.U + 2 * cb + site(k)));
+    u0[k] = cscale(ROT ? -1.0 : -0.5, __ldg(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
     u1[k] = cscale(-0.5, __ldg(a.U + 2 * cb + V + site(k)));
-    r[k] = ldg_spinor(a.b, cb + site(k));
+    r[k] = rot_in<ROT>(ldg_spinor(a.b, cb + site(k)));
     x[k].s0 = x[k].s1 = make_double2(0, 0);
     bb += spinor_norm2(r[k]);
   }
@@ -423,7 +423,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   const double target = a.tol * normb;
   if (normb == 0.0) {
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), x[k]);
+    for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(x[k]));
     if (tid == 0 && rank == 0) {
       a.iters[c] = 0;
       a.relres[c] = 0.0;
@@ -435,7 +435,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   const double t2 = target * target;
   const double t2lo = t2 * (1.0 - 4e-15), t2hi = t2 * (1.0 + 4e-15);
 
-  using Blk = SiteBlock<BX, BT>;
+  using Blk = std::conditional_t<ROT, SiteBlockRot<BX, BT>, SiteBlock<BX, BT>>;   // ROT: block_stencil.cuh
   // produce stage s: local planes, and the CTA's edge rows pushed to the
   // neighbouring CTAs' receive buffers
   auto produce = [&](auto dag, int s, const Spinor* v) {
@@ -501,7 +501,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   double rs = normb2;
   if (a.x0) {
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) x[k] = ldg_spinor(a.x0, cb + site(k));
+    for (int k = 0; k < SPT; ++k) x[k] = rot_in<ROT>(ldg_spinor(a.x0, cb + site(k)));
     apply(x, w, nullptr);
     double rr = 0.0;
 #pragma unroll
@@ -570,7 +570,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
       double tn2 = 0.0;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
-        w[k] = sp_sub(ldg_spinor(a.b, cb + site(k)), w[k]);
+        w[k] = sp_sub(rot_in<ROT>(ldg_spinor(a.b, cb + site(k))), w[k]);
         tn2 += spinor_norm2(w[k]);
       }
       publish(tn2, 2);
@@ -597,7 +597,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
     inv_rs = __drcp_rn(rs);
   }
 #pragma unroll
-  for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), x[k]);
+  for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(x[k]));
   if (tid == 0 && rank == 0) {
     a.iters[c] = status == 0 ? it : a.maxiter;
     a.relres[c] = status == 0 ? relres : fmin(best, sqrt(rs) / normb);

@@ -23,6 +23,8 @@
 // for y = RN(1/rs)), three dependent operations instead of a division.
 #pragma once
 
+#include <type_traits>
+
 #include "block_stencil.cuh"
 
 //
@@ -53,9 +55,15 @@ SCH_DEV Spinor res_ld_spinor(const double2* p, long long site) {
     return ldg_spinor(p, site);
 }
 
-template <int LC, int TC, int BX, int BT, int TSH, bool COH>
+template <int LC, int TC, int BX, int BT, int TSH, bool COH, bool ROT = false>
 SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
-  using Blk = SiteBlock<BX, BT>;
+  using Blk = std::conditional_t<ROT, SiteBlockRot<BX, BT>, SiteBlock<BX, BT>>;
+  // ROT: the solve runs in the sigma1-diagonal spin basis (block_stencil.cuh)
+  auto ld_b = [&](long long s) {
+    const Spinor v = res_ld_spinor<COH>(a.b, s);
+    return ROT ? spin_rot(v) : v;
+  };
+  auto st_x = [&](long long s, const Spinor& v) { st_spinor(a.x, s, ROT ? spin_unrot(v) : v); };
   constexpr int SPT = Blk::SPT;
   constexpr int NT = LC * TC / SPT;
   constexpr int NBT = TC / BT, NBX = LC / BX;
@@ -83,9 +91,9 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   double bb = 0.0;
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
-    u0[k] = cscale(-0.5, res_ld2<COH>(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
+    u0[k] = cscale(ROT ? -1.0 : -0.5, res_ld2<COH>(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
     u1[k] = cscale(-0.5, res_ld2<COH>(a.U + 2 * cb + V + site(k)));
-    r[k] = res_ld_spinor<COH>(a.b, cb + site(k));
+    r[k] = ld_b(cb + site(k));
     x[k].s0 = x[k].s1 = make_double2(0, 0);
     bb += spinor_norm2(r[k]);
   }
@@ -94,7 +102,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   const double target = a.tol * normb;
   if (normb == 0.0) {   // fermion.py:181-182, per chain
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), x[k]);
+    for (int k = 0; k < SPT; ++k) st_x(cb + site(k), x[k]);
     if (tid == 0) {
       a.iters[c] = 0;
       a.relres[c] = 0.0;
@@ -165,7 +173,10 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   double rs = normb2;   // r = b exactly: the same sum as ||b||^2 (fermion.py:186,191)
   if (a.x0) {
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) x[k] = res_ld_spinor<COH>(a.x0, cb + site(k));
+    for (int k = 0; k < SPT; ++k) {
+      x[k] = res_ld_spinor<COH>(a.x0, cb + site(k));
+      if constexpr (ROT) x[k] = spin_rot(x[k]);
+    }
     normal_op(x, w);
     double rr = 0.0;
 #pragma unroll
@@ -227,7 +238,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
       double tn2 = 0.0;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
-        w[k] = sp_sub(res_ld_spinor<COH>(a.b, cb + site(k)), w[k]);
+        w[k] = sp_sub(ld_b(cb + site(k)), w[k]);
         tn2 += spinor_norm2(w[k]);
       }
       tn2 = block_sum<NT>(tn2, red[2]);
@@ -235,7 +246,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
       if (!repl || tn <= target) best = tn / normb;
       if (tn <= target) {
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), x[k]);
+        for (int k = 0; k < SPT; ++k) st_x(cb + site(k), x[k]);
         if (tid == 0) {
           a.iters[c] = it;
           a.relres[c] = tn / normb;
@@ -258,7 +269,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
     inv_rs = __drcp_rn(rs);
   }
 #pragma unroll
-  for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), x[k]);
+  for (int k = 0; k < SPT; ++k) st_x(cb + site(k), x[k]);
   if (tid == 0) {
     a.iters[c] = a.maxiter;
     a.relres[c] = fmin(best, sqrt(rs) / normb);
@@ -266,8 +277,8 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   }
 }
 
-template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0>
+template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0, bool ROT = false>
 __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs a) {
   extern __shared__ double2 sm[];
-  cg_resblk_run<LC, TC, BX, BT, TSH, false>(a, blockIdx.x, (long long)blockIdx.x * LC * TC, sm);
+  cg_resblk_run<LC, TC, BX, BT, TSH, false, ROT>(a, blockIdx.x, (long long)blockIdx.x * LC * TC, sm);
 }

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .lattice import as_links, as_spinor, geom_of, n_chains, squeeze_chain
+from .lattice import as_links, as_spinor, geom_of, kick, n_chains, squeeze_chain
 
 DEFAULT_TOL = 1e-12          # fermion.py:28
 DEFAULT_MAXITER = 10_000     # fermion.py:29
@@ -477,7 +477,9 @@ def z_pair(op: WilsonDirac, weight, chi, xi, tol: float = DEFAULT_TOL,
     """Z1 = D^{-dag} b1, Z2 = D^{-1}(b2 + Z1); two inversions (fermion.py:386-394)."""
     b1, b2 = weighted_w_sums(op, weight, chi, xi)
     z1, r1 = solve_dirac_dagger(op, b1, tol, counter=counter, exact=exact, stop=stop, check=check)
-    z2, r2 = solve_dirac(op, b2 + z1, tol, counter=counter, exact=exact, stop=stop, check=check)
+    # b2 + Z1 on our kick kernel over the real view: b2 - (-1*Z1) == b2 + Z1 exactly
+    b2z1 = torch.view_as_complex(kick(torch.view_as_real(b2), torch.view_as_real(z1), -1.0))
+    z2, r2 = solve_dirac(op, b2z1, tol, counter=counter, exact=exact, stop=stop, check=check)
     if infos is not None:
         infos.extend(r._info for r in (r1, r2) if r._info is not None)
     return z1, z2

@@ -27,7 +27,7 @@ from .fermion import SolverError
 from .integrators import (FG_KICK_SIGN, INVERSIONS_PER_STEP, IntegratorSpec, MdState, TrajectoryResult,
                           integrate_trajectory)
 from .lattice import (DeviceRng, LatticeGeom, NumpyDeviceRng, as_links, as_spinor, cold_start,
-                      kinetic_energy,
+                      kick, kinetic_energy,
                       sample_momenta)
 
 log = logging.getLogger("schwinger")
@@ -72,8 +72,8 @@ def hamiltonian(state: MdState) -> torch.Tensor:
     kin = kinetic_energy(state.p)
     s_g = gauge_action(state.q, state.beta)
     _, _, xi = state.solve_pair()
-    s_f = spinor_dot(state.eta, xi).real
-    return (kin + s_g) + s_f
+    s_f = spinor_dot(state.eta, xi).real.contiguous()
+    return kick(kick(kin, s_g, -1.0), s_f, -1.0)   # (kin + s_g) + s_f, on our kernel
 
 
 def metropolis(dh: float, rng) -> bool:
@@ -118,7 +118,7 @@ def hmc_update(q, config: HmcConfig, rng, counter: InversionCounter | None = Non
     wall = time.perf_counter() - t0
     h_end = hamiltonian(state)
     state.check_solves()
-    dh = float((h_end - h_start).item())
+    dh = float(kick(h_end, h_start, 1.0).item())
     accepted = metropolis(dh, rng)
     stats = TrajectoryStats(dh=dh, accepted=accepted, inversions=result.inversions,
                             n_steps=result.n_steps, wall_time=wall)
@@ -151,7 +151,7 @@ def measure_dh(q0, config: HmcConfig, rng, n_samples: int | None = None,
     wall = time.perf_counter() - t0
     h_end = hamiltonian(state)
     state.check_solves()
-    dh = (h_end - h_start).cpu().numpy().astype(np.float64)
+    dh = kick(h_end, h_start, 1.0).cpu().numpy().astype(np.float64)
     ad = np.abs(dh)
     mean_abs = float(np.mean(ad))
     stderr = float(np.std(ad, ddof=1) / np.sqrt(n)) if n > 1 else 0.0
@@ -351,7 +351,7 @@ def _ensemble_update(q, config, rngs, device_rng, counter, reuse_solves, sync):
         h_start = hamiltonian(state)
         result = integrate_trajectory(state, _spec_of(config), config.tau, check=sync)
         h_end = hamiltonian(state)
-        dh_dev = h_end - h_start
+        dh_dev = kick(h_end, h_start, 1.0)
     if device_rng is not None:
         if isinstance(device_rng, NumpyDeviceRng):
             acc = device_rng.metropolis(dh_dev)
