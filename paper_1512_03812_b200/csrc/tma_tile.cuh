@@ -56,6 +56,46 @@ SCH_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;"
 
 SCH_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
 
+// res_consume with the t-direction exports passed in (warp shuffles) instead
+// of read from the E planes 2/3; same arithmetic, same order.
+template <bool DAG>
+SCH_DEV Spinor res_consume_tsh(const double2* __restrict__ E, int V, const Spinor& v, double2 u0,
+                               double2 u1, int nxp, int nxm, double2 f1n, double2 b1n,
+                               double diag) {
+  const double2 hf0 = cmul(u0, E[nxp]);
+  const double2 hb0 = E[V + nxm];
+  const double2 hf1 = cmul(u1, f1n);
+  const double2 hb1 = b1n;
+  double2 o0 = cadd(cadd(cadd(hf0, hb0), hf1), hb1);
+  double2 o1 = DAG ? cadd(csub(hf0, hb0), cmuli(csub(hf1, hb1)))
+                   : cadd(csub(hb0, hf0), cmuli(csub(hb1, hf1)));
+  Spinor r;
+  r.s0 = make_double2(diag * v.s0.x - 0.5 * o0.x, diag * v.s0.y - 0.5 * o0.y);
+  r.s1 = make_double2(diag * v.s1.x - 0.5 * o1.x, diag * v.s1.y - 0.5 * o1.y);
+  return r;
+}
+
+// x-direction exports to E (planes 0/1); the t-direction ones returned
+template <bool DAG>
+SCH_DEV void res_produce_x(double2* __restrict__ E, int V, int s, const Spinor& v, double2 u0,
+                           double2 u1, double2& f1, double2& b1) {
+  if (!DAG) {
+    E[s] = wminus0(v);
+    E[V + s] = cmulc(u0, wplus0(v));
+    f1 = wminus1(v);
+    b1 = cmulc(u1, wplus1(v));
+  } else {
+    E[s] = wplus0(v);
+    E[V + s] = cmulc(u0, wminus0(v));
+    f1 = wplus1(v);
+    b1 = cmulc(u1, wminus1(v));
+  }
+}
+
+SCH_DEV double2 tma_shfl_d2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
 // Shared-memory footprint of one pipeline stage and of the whole kernel.
 template <int TX, int T_, int MODE>
 struct TmaGeom {
@@ -102,11 +142,17 @@ SCH_DEV void tma_issue_tile(const TileArgs& a, int w, char* st, uint64_t* bar) {
   }
 }
 
+#ifndef SCH_TMA_TSH
+#define SCH_TMA_TSH 1
+#endif
+constexpr bool tma_tsh_enabled = SCH_TMA_TSH != 0;   // build with -DSCH_TMA_TSH=0 for the SMEM t-faces
+
 template <int TX, int T_, int MODE, int NT, int STAGES, int MINB = 1>
 __global__ void __launch_bounds__(NT, MINB) k_normal_tma(TileArgs a) {
   using G = TmaGeom<TX, T_, MODE>;
   constexpr int RX = G::RX, RT = T_, NR = G::NR;
   constexpr int CPT = (NR + NT - 1) / NT;
+  constexpr bool TSH = T_ <= 32 && 32 % T_ == 0 && NT % 32 == 0 && NR % 32 == 0 && tma_tsh_enabled;
   extern __shared__ __align__(128) char smem[];
   char* ring = smem;                                            // STAGES x STAGE_B
   double2* E = reinterpret_cast<double2*>(smem + STAGES * G::STAGE_B);
@@ -148,8 +194,15 @@ __global__ void __launch_bounds__(NT, MINB) k_normal_tma(TileArgs a) {
     mbar_wait(&bars[stage], parity);
 
     // ---- phase A: owner reads its cells from the stage, exports projections
+    // TSH: a time row (T_ <= 32 cells) lies inside one warp, lane % T_ = t,
+    // so the t-direction exports move by warp shuffle and only the x ones
+    // go through shared memory (E planes 0/1).
     Spinor v[CPT], t[CPT];
     double2 u0[CPT], u1[CPT];
+    double2 tf[CPT], tb[CPT];
+    const int lane = threadIdx.x & 31;
+    const int lrow = lane & ~(T_ - 1), lt = lane & (T_ - 1);
+    const int lane_tp = lrow | ((lt + 1) & (T_ - 1)), lane_tm = lrow | ((lt + T_ - 1) & (T_ - 1));
 #pragma unroll
     for (int j = 0; j < CPT; ++j) {
       const int k = threadIdx.x + j * NT;
@@ -162,7 +215,10 @@ __global__ void __launch_bounds__(NT, MINB) k_normal_tma(TileArgs a) {
       }
       u0[j] = sU0[k];
       u1[j] = sU1[k];
-      if (active) res_produce<false>(E, NR, k, v[j], u0[j], u1[j]);
+      if (active) {
+        if constexpr (TSH) res_produce_x<false>(E, NR, k, v[j], u0[j], u1[j], tf[j], tb[j]);
+        else res_produce<false>(E, NR, k, v[j], u0[j], u1[j]);
+      }
     }
     __syncthreads();   // stage fully consumed; exports visible
     if (threadIdx.x == 0) {
@@ -177,12 +233,21 @@ __global__ void __launch_bounds__(NT, MINB) k_normal_tma(TileArgs a) {
 #pragma unroll
       for (int j = 0; j < CPT; ++j) {
         const int k = threadIdx.x + j * NT;
-        if (k >= NR) continue;
+        if (k >= NR) continue;   // warp-uniform (NR % 32 == 0 under TSH)
+        double2 f1n, b1n;
+        if constexpr (TSH) {     // every lane of the warp takes part
+          f1n = tma_shfl_d2(tf[j], lane_tp);
+          b1n = tma_shfl_d2(tb[j], lane_tm);
+        }
         const int ri = k / RT, rj = k - (k / RT) * RT;
         if (ri < 1 || ri >= RX - 1) continue;
-        const int jp = rj + 1 == RT ? 0 : rj + 1, jm = rj == 0 ? RT - 1 : rj - 1;
-        t[j] = res_consume<false>(E, NR, v[j], u0[j], u1[j], k + RT, k - RT, ri * RT + jp,
-                                  ri * RT + jm, a.diag);
+        if constexpr (TSH) {
+          t[j] = res_consume_tsh<false>(E, NR, v[j], u0[j], u1[j], k + RT, k - RT, f1n, b1n, a.diag);
+        } else {
+          const int jp = rj + 1 == RT ? 0 : rj + 1, jm = rj == 0 ? RT - 1 : rj - 1;
+          t[j] = res_consume<false>(E, NR, v[j], u0[j], u1[j], k + RT, k - RT, ri * RT + jp,
+                                    ri * RT + jm, a.diag);
+        }
       }
     }
     __syncthreads();
@@ -192,8 +257,12 @@ __global__ void __launch_bounds__(NT, MINB) k_normal_tma(TileArgs a) {
         const int k = threadIdx.x + j * NT;
         if (k >= NR) continue;
         const int ri = k / RT;
-        if (ri < 1 || ri >= RX - 1) continue;
-        res_produce<true>(E, NR, k, t[j], u0[j], u1[j]);
+        if (ri < 1 || ri >= RX - 1) {
+          if constexpr (TSH) tf[j] = tb[j] = make_double2(0.0, 0.0);   // never consumed
+          continue;
+        }
+        if constexpr (TSH) res_produce_x<true>(E, NR, k, t[j], u0[j], u1[j], tf[j], tb[j]);
+        else res_produce<true>(E, NR, k, t[j], u0[j], u1[j]);
       }
     }
     __syncthreads();
@@ -204,11 +273,21 @@ __global__ void __launch_bounds__(NT, MINB) k_normal_tma(TileArgs a) {
       for (int j = 0; j < CPT; ++j) {
         const int k = threadIdx.x + j * NT;
         if (k >= NR) continue;
+        double2 f1n, b1n;
+        if constexpr (TSH) {
+          f1n = tma_shfl_d2(tf[j], lane_tp);
+          b1n = tma_shfl_d2(tb[j], lane_tm);
+        }
         const int ri = k / RT, rj = k - (k / RT) * RT;
         if (ri < 2 || ri >= RX - 2 || x0 + ri - 2 >= L) continue;
-        const int jp = rj + 1 == RT ? 0 : rj + 1, jm = rj == 0 ? RT - 1 : rj - 1;
-        Spinor r = res_consume<true>(E, NR, t[j], u0[j], u1[j], k + RT, k - RT, ri * RT + jp,
-                                     ri * RT + jm, a.diag);
+        Spinor r;
+        if constexpr (TSH) {
+          r = res_consume_tsh<true>(E, NR, t[j], u0[j], u1[j], k + RT, k - RT, f1n, b1n, a.diag);
+        } else {
+          const int jp = rj + 1 == RT ? 0 : rj + 1, jm = rj == 0 ? RT - 1 : rj - 1;
+          r = res_consume<true>(E, NR, t[j], u0[j], u1[j], k + RT, k - RT, ri * RT + jp,
+                                ri * RT + jm, a.diag);
+        }
         const long long site = cbase + (long long)(x0 + ri - 2) * RT + rj;
         if (MODE == MODE_X) {
           Spinor bb = ld256_spinor_nc(a.bvec, site);
