@@ -77,6 +77,46 @@ SCH_DEV Spinor res_consume(const double2* __restrict__ E, int V, const Spinor& v
   return r;
 }
 
+// res_consume with the t-direction exports passed in (warp shuffles) instead
+// of read from the E planes 2/3; same arithmetic, same order.
+template <bool DAG>
+SCH_DEV Spinor res_consume_tsh(const double2* __restrict__ E, int V, const Spinor& v, double2 u0,
+                               double2 u1, int nxp, int nxm, double2 f1n, double2 b1n,
+                               double diag) {
+  const double2 hf0 = cmul(u0, E[nxp]);
+  const double2 hb0 = E[V + nxm];
+  const double2 hf1 = cmul(u1, f1n);
+  const double2 hb1 = b1n;
+  double2 o0 = cadd(cadd(cadd(hf0, hb0), hf1), hb1);
+  double2 o1 = DAG ? cadd(csub(hf0, hb0), cmuli(csub(hf1, hb1)))
+                   : cadd(csub(hb0, hf0), cmuli(csub(hb1, hf1)));
+  Spinor r;
+  r.s0 = make_double2(diag * v.s0.x - 0.5 * o0.x, diag * v.s0.y - 0.5 * o0.y);
+  r.s1 = make_double2(diag * v.s1.x - 0.5 * o1.x, diag * v.s1.y - 0.5 * o1.y);
+  return r;
+}
+
+// x-direction exports to E (planes 0/1); the t-direction ones returned
+template <bool DAG>
+SCH_DEV void res_produce_x(double2* __restrict__ E, int V, int s, const Spinor& v, double2 u0,
+                           double2 u1, double2& f1, double2& b1) {
+  if (!DAG) {
+    E[s] = wminus0(v);
+    E[V + s] = cmulc(u0, wplus0(v));
+    f1 = wminus1(v);
+    b1 = cmulc(u1, wplus1(v));
+  } else {
+    E[s] = wplus0(v);
+    E[V + s] = cmulc(u0, wminus0(v));
+    f1 = wplus1(v);
+    b1 = cmulc(u1, wminus1(v));
+  }
+}
+
+SCH_DEV double2 tile_shfl_d2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
 // consumer split in two: gather the four neighbour exports (issue all
 // shared-memory loads first), then combine
 struct Hops {
