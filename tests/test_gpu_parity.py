@@ -382,3 +382,46 @@ def test_wrap_angles_bit_exact_stress(sw):
     got = sw.wrap_angles(vals).cpu().numpy()
     want = O.wrap_angles(vals)
     assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+
+
+_BASIS_SNIPPET = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_1512_03812_b200 as sw
+from paper_1512_03812_b200 import fermion as F
+out = {}
+for L, B in ((16, 6), (32, 3), (64, 2)):
+    rng = np.random.default_rng(100 + L)
+    q = rng.uniform(-np.pi, np.pi, (B, 2, L, L))
+    b = rng.standard_normal((B, L, L, 2)) + 1j * rng.standard_normal((B, L, L, 2))
+    op = sw.WilsonDirac(q, 0.1)
+    x, info = F.cg_solve(op, b, 1e-10, stop="per_chain")
+    out[f"x{L}"] = x.cpu().numpy()
+    out[f"it{L}"] = info.iters_dev.cpu().numpy()
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_resident_cg_spin_basis_matches_reference_basis(tmp_path):
+    """The resident engines solve in the sigma1-diagonal spin basis by default
+    (block_stencil.cuh SiteBlockRot); SCH_RESBLK_ROT=0 runs the reference
+    basis.  Both must give the same solutions (<= 1e-12 relative, the CG
+    tolerance bar) and the same iteration counts on the 16^2 / 32^2 block
+    kernels and the 64^2 cluster kernel.  The switch is read once per
+    process, so each basis runs in its own interpreter."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for rot in ("0", "1"):
+        path = tmp_path / f"rot{rot}.npz"
+        env = dict(os.environ, SCH_RESBLK_ROT=rot)
+        subprocess.run([sys.executable, "-c", _BASIS_SNIPPET, root, str(path)], check=True, env=env,
+                       timeout=300)
+        res[rot] = np.load(path)
+    for L in (16, 32, 64):
+        a, b = res["0"][f"x{L}"], res["1"][f"x{L}"]
+        assert rel_err(b, a) <= TOL_OP, (L, rel_err(b, a))
+        np.testing.assert_array_equal(res["0"][f"it{L}"], res["1"][f"it{L}"])
