@@ -55,6 +55,42 @@ SCH_DEV Spinor res_ld_spinor(const double2* p, long long site) {
     return ldg_spinor(p, site);
 }
 
+// Per-iteration CTA sums with a shorter dependent chain than block_sum: three
+// xor-butterfly levels leave each lane holding the sum of its 8-lane residue
+// class; lanes 0..3 of every warp publish those (4 per warp), and after the
+// barrier every thread adds the 4*NW slots as a fixed pairwise tree (the same
+// value in every thread).
+template <int NW>
+SCH_DEV void part4_put(double v, double* slot) {
+  v += __shfl_xor_sync(0xffffffffu, v, 16);
+  v += __shfl_xor_sync(0xffffffffu, v, 8);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  const int lane = threadIdx.x & 31;
+  if (lane < 4) slot[(threadIdx.x >> 5) * 4 + lane] = v;
+}
+template <int NW>
+SCH_DEV double part4_sum(const double* slot) {
+  constexpr int N = 4 * NW;
+  double a[N / 2];
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) {
+    const double2 v = reinterpret_cast<const double2*>(slot)[i];
+    a[i] = v.x + v.y;
+  }
+#pragma unroll
+  for (int w = N / 4; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int i = 0; i < w; ++i) a[i] = a[2 * i] + a[2 * i + 1];
+  }
+  return a[0];
+}
+template <int NW>
+SCH_DEV double part4_block_sum(double v, double* slot) {
+  part4_put<NW>(v, slot);
+  __syncthreads();
+  return part4_sum<NW>(slot);
+}
+
 template <int LC, int TC, int BX, int BT, int TSH, bool COH, bool ROT = false>
 SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   using Blk = std::conditional_t<ROT, SiteBlockRot<BX, BT>, SiteBlock<BX, BT>>;
@@ -75,6 +111,10 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   // plane offsets inside one stage
   constexpr int O0 = 0, O1 = BT * NT, O2 = 2 * BT * NT, O3 = (2 * BT + BX) * NT;
   __shared__ double red[3][NW];
+  // per-iteration sums: part4_* for two-warp CTAs (16^2: 2.02 -> 1.98 ns per
+  // chain-iteration); wider CTAs keep the full butterfly (32^2 with part4: 9.17 -> 10.19)
+  constexpr bool P4 = NW <= 2;
+  __shared__ __align__(16) double red4[2][4 * NW];
   double2* E0 = sm;
   double2* E1 = sm + PL;
   const int tid = threadIdx.x;
@@ -203,14 +243,23 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
 #pragma unroll
       for (int k = 0; k < SPT; ++k) dd += spinor_norm2(t[k]);
       stage_pre(T{}, E1, t, w);
-      dd = warp_sum(dd);
-      if ((tid & 31) == 0) red[0][tid >> 5] = dd;
+      if constexpr (P4) {
+        part4_put<NW>(dd, red4[0]);
+      } else {
+        dd = warp_sum(dd);
+        if ((tid & 31) == 0) red[0][tid >> 5] = dd;
+      }
       __syncthreads();
       stage_post(T{}, E1, w);
     }
-    double den = red[0][0];
+    double den;
+    if constexpr (P4) {
+      den = part4_sum<NW>(red4[0]);
+    } else {
+      den = red[0][0];
 #pragma unroll
-    for (int q = 1; q < NW; ++q) den += red[0][q];
+      for (int q = 1; q < NW; ++q) den += red[0][q];
+    }
     const double alpha = den > 0.0 ? rs / den : 0.0;
     const bool repl = (it % kResReplace) == 0;
     double rsn = 0.0;
@@ -225,7 +274,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
     double rs_new = 0.0;
     bool check = true;
     if (!repl) {
-      rs_new = block_sum<NT>(rsn, red[1]);
+      rs_new = P4 ? part4_block_sum<NW>(rsn, red4[1]) : block_sum<NT>(rsn, red[1]);
       check = rs_new <= t2lo;
       if (!check && rs_new <= t2hi) {   // inside the band: the exact test (asm keeps
         double sq;                      // the compiler from hoisting the sqrt)
