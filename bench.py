@@ -60,8 +60,8 @@ CG_KERNELS = {
     "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread,t-faces by warp shuffle,"
                         "sigma1-diagonal spin basis> (per-chain CG, one 64-thread CTA per chain, "
                         "4 CTAs/SM)",
-                 dram_per_site=(134.253568e6 + 35.483904e6) / (8192 * 256),
-                 fp64_pipe_active=0.628,
+                 dram_per_site=(134.252288e6 + 35.547392e6) / (8192 * 256),
+                 fp64_pipe_active=0.652,
                  source="profiles/r01/ncu_full_k_cg_resblk_rot.txt"),
     "cfg3_mega": dict(kernel="k_traj_anfg16 (trajectory megakernel: one 64-thread CTA per 16x16 "
                              "chain runs H(start), the 17 resident-CG solves, forces, FG terms, "
