@@ -262,15 +262,23 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
     }
     const double alpha = den > 0.0 ? rs / den : 0.0;
     const bool repl = (it % kResReplace) == 0;
-    double rsn = 0.0;
+    double nrm[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       x[k] = sp_fma(alpha, p[k], x[k]);
       if (!repl) {
         r[k] = sp_fma(-alpha, w[k], r[k]);
-        rsn += spinor_norm2(r[k]);
+        nrm[k] = spinor_norm2(r[k]);
       }
     }
+    // the thread's sites summed pairwise (a shorter chain ahead of the
+    // butterfly than a running sum)
+#pragma unroll
+    for (int h = 1; h < SPT; h *= 2) {
+#pragma unroll
+      for (int k = 0; k + h < SPT; k += 2 * h) nrm[k] += nrm[k + h];
+    }
+    const double rsn = repl ? 0.0 : nrm[0];
     double rs_new = 0.0;
     bool check = true;
     if (!repl) {
