@@ -322,13 +322,18 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.window = None
+
+    def mark(self, t0, t1):
+        """Wall-clock bounds of the timed region: only samples inside count."""
+        self.window = (t0, t1)
 
     def start(self):
         if os.environ.get("SCH_NO_CLOCKS"):
@@ -351,8 +356,17 @@ class ClockSampler:
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 6:
+            if len(parts) < 7:
                 continue
+            if self.window is not None:
+                try:   # e.g. "2026/10/20 10:42:16.123" (local time)
+                    stamp, frac = parts[0].rsplit(".", 1)
+                    ts = time.mktime(time.strptime(stamp, "%Y/%m/%d %H:%M:%S")) + float("0." + frac)
+                    if not self.window[0] - 0.25 <= ts <= self.window[1] + 0.25:
+                        continue
+                except ValueError:
+                    pass
+            parts = parts[1:]
             try:
                 sm.append(float(parts[0]))
                 mx = float(parts[1])
@@ -730,9 +744,14 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
+    # nvidia-smi's own start-up (NVML init) contends with this process's
+    # launches: start it before the timed region and keep only its samples
+    # from inside the region (ClockSampler.mark)
+    clocks.start()
+    time.sleep(0.75)
     barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    t_wall0 = time.time()
     F.CG_PROFILE = []
     launches0 = _lib.launch_count()
     acc, dhs = [], []
@@ -748,6 +767,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     launches = _lib.launch_count() - launches0
+    clocks.mark(t_wall0, time.time())
     clk = clocks.stop()
     prof, F.CG_PROFILE = F.CG_PROFILE, None
     ms = e0.elapsed_time(e1)
@@ -797,10 +817,12 @@ def run_ours(args):
         # Copies run on a copy stream, double-buffered, so step k+1's upload
         # and step k's download overlap the neighbouring step's compute (a
         # pipelined client; every byte still crosses PCIe inside the window).
+        # The host reads step k-2's results after issuing step k (two steps
+        # queued, as the device-timed leg), so a host stall does not idle the GPU.
         q_host = [qi.cpu().pin_memory() for qi in qs]
         q_back = [torch.empty_like(h).pin_memory() for h in q_host]
         h2d = sum(h.numel() for h in q_host) * 8
-        steps_e2e = max(2, args.steps // 2)
+        steps_e2e = max(4, args.steps)
         copy = [torch.cuda.Stream() for _ in streams]
         din = [[torch.empty_like(qi) for _ in range(2)] for qi in qs]
         ev_in = [[torch.cuda.Event() for _ in range(2)] for _ in qs]
@@ -822,7 +844,7 @@ def run_ours(args):
         for i in range(S):
             copy[i].wait_stream(main)
             upload(i, 0)
-        prev_pend = []
+        queued = []   # per step: the pendings of its chains' dH / accept
         for k in range(steps_e2e):
             slot = k % 2
             pend = []
@@ -840,11 +862,13 @@ def run_ours(args):
                     out.record_stream(copy[i])
                     q_back[i].copy_(out, non_blocking=True)
                 pend.append(p)
-            for p in prev_pend:   # step k-1's dH / accept, read while step k runs
+            queued.append(pend)
+            if len(queued) > 2:   # step k-2's dH / accept, read while k-1 and k are queued
+                for p in queued.pop(0):
+                    p.resolve()
+        for pend in queued:
+            for p in pend:
                 p.resolve()
-            prev_pend = pend
-        for p in prev_pend:
-            p.resolve()
         for i, stm in enumerate(streams):
             main.wait_stream(stm)
             main.wait_stream(copy[i])
