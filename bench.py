@@ -3,17 +3,20 @@
 
 Workload (BASELINE.json configs[2], "cfg3"): independent 16x16 chains,
 beta=2.0, m0=0.1, tau=1, adapted nested force-gradient (the paper's scheme),
-micro_per_call=2, CG tolerance 1e-10, complex128, hot start; 8192 chains per
-GPU (weak scaling across ranks, no collective on the data path; one NCCL
-all-gather of per-chain dH/accept at the end).  A "step" is one full HMC
-update of every chain (heatbaths, H, trajectory, H, Metropolis).
+micro_per_call=2, CG tolerance 1e-10, complex128, hot start; 8192 chains in
+the ensemble, split across the ranks (strong scaling, configs[2]; --weak keeps
+--chains per GPU), no collective on the data path, one NCCL all-gather of
+per-chain dH/accept at the end.  A "step" is one full HMC update of every
+chain (heatbaths, H, trajectory, H, Metropolis).  `--gpus N` outside torchrun
+starts the N ranks itself (torch.distributed.run, 127.0.0.1).
 
 Also reported on the same line:
   roofline   : the dominant kernel (the resident per-chain CG) against the
-               HBM roofline on the SURVEY §8(d) algorithmic model (352 B per
-               site per CG iteration) — "effective", since the CG working set
-               lives in shared memory/registers — plus its FP64 rate against
-               a live FP64 FMA probe;
+               FP64 roofline (SMs x 128 flop/clk x max clock) on the SURVEY
+               §8(d) algorithmic model (152 flop per site per CG iteration),
+               with a live FP64 FMA probe beside it; its working set lives in
+               registers/shared memory, so the 352 B/site/iteration streaming
+               model's HBM rate is only a secondary "hbm_effective" field;
   stencil    : BASELINE configs[1] ("cfg2"): 4096 x 32^2, fused D^dag D GB/s at
                96 B/site and the streaming CG to 1e-10 at 352 B/site/iteration;
   cpu_baseline: the CPU oracle port (per-chain hmc_update) on the host cores;
@@ -99,11 +102,16 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="cfg3",
                     help="cfg3 (default, the bench line) or cfg4 (64^2 light-fermion ensemble)")
-    ap.add_argument("--chains", type=int, default=None, help="chains per GPU")
-    ap.add_argument("--strong", action="store_true",
-                    help="strong scaling: --chains is the ensemble total, split across the ranks "
-                         "(BASELINE configs[2] reads '8192 chains sharded across 1/2/4/8 GPUs'); "
-                         "default weak scaling: --chains per GPU")
+    ap.add_argument("--chains", type=int, default=None,
+                    help="the ensemble total, split across the ranks (strong scaling, the "
+                         "default: BASELINE configs[2] reads '8192 chains sharded across "
+                         "1/2/4/8 GPUs', configs[3] '1024 chains ... sharded across 8 GPUs'); "
+                         "with --weak: chains per GPU")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: --chains per GPU, the ensemble grows with the ranks")
+    ap.add_argument("--therm", type=int, default=0,
+                    help="untimed updates before the warm-up (a thermalized start; cfg4's CG "
+                         "iterations grow as its chains order)")
     ap.add_argument("--outer", type=int, default=None, help="outer (fermion) steps per trajectory")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
@@ -403,6 +411,21 @@ def fp64_probe(torch, _lib):
     return best
 
 
+def fp64_peak_theoretical(torch):
+    """FP64 peak of the device: SMs x 64 FP64 FMA lanes x 2 flop x the max SM
+    clock (MEASURED_PEAKS.json's sm_max_mhz; B200: 148 x 128 x 1.965 GHz =
+    37.2 TFLOP/s).  FP64 is not in MEASURED_PEAKS.json, so this is the
+    datasheet-class arithmetic peak; the live FMA probe is reported beside it."""
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    try:
+        mhz = float(json.loads(PEAKS_PATH.read_text())["sm_max_mhz"])
+        kind = "theoretical: SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz (MEASURED_PEAKS.json)"
+    except Exception:
+        mhz = 1965.0
+        kind = "theoretical: SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (B200 max SM clock)"
+    return sms * 128.0 * mhz * 1e6 / 1e12, kind
+
+
 def stencil_bench(torch, sw, _lib, hbm_peak):
     """cfg2: 4096 x 32^2, fused D^dag D and the CG to 1e-10."""
     from paper_1512_03812_b200 import fermion as F
@@ -680,8 +703,8 @@ def run_ours(args):
             stencil["ddagd"]["cpu_baseline"] = cpu_stencil
 
     from paper_1512_03812_b200.ensemble import gather_observables, shard_chains, summarize
-    # weak scaling (default): chains per GPU fixed; --strong: the ensemble total fixed
-    shard = shard_chains(args.chains if args.strong else args.chains * world, world, rank)
+    # strong scaling (default): the ensemble total fixed; --weak: chains per GPU fixed
+    shard = shard_chains(args.chains * world if args.weak else args.chains, world, rank)
     chains = shard.count
     cfg = sw.HmcConfig(h=1.0 / args.outer, **CFG3)
     geom = sw.LatticeGeom(cfg.L, cfg.T)
@@ -738,9 +761,10 @@ def run_ours(args):
     # (tools/step_jitter.py), so collect once here and keep it off while timing.
     gc.collect()
     gc.disable()
-    # warm up in the timed region's own pattern (steps queued ahead), so the
-    # caching allocator already holds the buffers of every in-flight step
-    sts = run_steps(args.warmup)
+    # an optional thermalization, then the warm-up in the timed region's own
+    # pattern (steps queued ahead), so the caching allocator already holds the
+    # buffers of every in-flight step
+    sts = run_steps(args.therm + args.warmup)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -798,7 +822,9 @@ def run_ours(args):
     cg_bytes = 352.0 * V * cg_iters
     cg_flops = 152.0 * V * cg_iters
     achieved = cg_bytes / (cg_ms * 1e-3) / 1e9
-    fp64_peak = fp64_probe(torch, _lib)
+    fp64_probe_peak = fp64_probe(torch, _lib)
+    fp64_peak, fp64_kind = fp64_peak_theoretical(torch)
+    fp64_achieved = cg_flops / (cg_ms * 1e-3) / 1e12
     # the megakernel runs every solve of a trajectory in one launch: 1 + 4n
     solves_per_traj = (1 + 4 * max(1, round(cfg.tau / cfg.h))) if mega else n_solves / args.steps
 
@@ -899,7 +925,7 @@ def run_ours(args):
         line = {
             "metric": "HMC trajectories/s", "value": value, "unit": "chain-trajectories/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+            "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
             "vs_baseline": None,
             "dtype": "f64/c128",
             "data": "synthetic: hot start + heatbaths drawn on device from the reference's own "
@@ -915,32 +941,43 @@ def run_ours(args):
                        "exp_minus_dh": ens["exp_minus_dh"],
                        "cg_solves_per_traj": solves_per_traj,
                        "inversions_per_traj_reference_convention": st.inversions,
-                       "cg_iterations_per_chain_traj": cg_iters / (chains * args.steps)},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak,
+                       "cg_iterations_per_chain_traj": cg_iters / (chains * args.steps),
+                       "cg_iterations_per_solve": cg_iters / max(1, chains * n_solves),
+                       "therm_updates_before_warmup": args.therm},
+            "roofline": {"bound": "fp64", "achieved": fp64_achieved, "peak": fp64_peak,
+                         "unit": "TFLOP/s", "frac": fp64_achieved / fp64_peak,
                          "traffic": (None if kinfo["dram_per_site"] is None
                                      else kinfo["dram_per_site"] * V * chains),
+                         "traffic_unit": "bytes per launch",
                          "traffic_source": "dram__bytes_read.sum+dram__bytes_write.sum of one "
                                            f"launch (ncu --set full, {kinfo['source']}), per "
                                            "site, x sites of one launch here",
-                         "algorithmic_bytes_per_launch": cg_bytes / max(1, n_solves),
-                         "peak_kind": peak_kind,
                          "kernel": kinfo["kernel"],
-                         "bytes_model": "352 B/site/CG-iteration (SURVEY 8(d)), "
-                                        f"{V} sites x {cg_iters} chain-iterations",
-                         "effective": True,
-                         "note": "working set is SMEM/register resident; true bound is FP64 "
-                                 "issue / shared-memory bandwidth" + (
+                         "flops_model": "152 flop/site/CG-iteration (SURVEY 8(d): 112 D^dag D + "
+                                        f"40 dots/axpys), {V} sites x {cg_iters} "
+                                        "chain-iterations, / the union of the CG launch intervals "
+                                        "(CUDA events on the launching stream)",
+                         "algorithmic_flops_per_launch": cg_flops / max(1, n_solves),
+                         "peak_kind": fp64_kind,
+                         "fp64_peak_probe": fp64_probe_peak,
+                         "frac_of_probe": fp64_achieved / fp64_probe_peak,
+                         "fp64_pipe_active_ncu": kinfo["fp64_pipe_active"],
+                         "note": "the solve's working set lives in registers and shared memory, "
+                                 "so FP64 issue, not HBM, bounds it; the achieved rate counts the "
+                                 "152-flop model, while the kernel issues ~96 FP64 instructions "
+                                 "per site-iteration (sigma1-diagonal spin basis): ncu's FP64 "
+                                 "pipe-active fraction is the issue-rate measure" + (
                                      "; the megakernel's time also holds its non-CG phases "
                                      "(forces, FG terms, inner leapfrogs, H)" if mega else ""),
-                         "fp64_tflops": cg_flops / (cg_ms * 1e-3) / 1e12,
-                         "fp64_peak_tflops_probe": fp64_peak,
-                         "fp64_frac": cg_flops / (cg_ms * 1e-3) / 1e12 / fp64_peak,
-                         "fp64_pipe_active_ncu": kinfo["fp64_pipe_active"],
-                         "fp64_note": "fp64_frac counts the 152 flop/site model; the kernel "
-                                      "issues ~96 FP64 instructions per site-iteration (sigma1-diagonal basis), and "
-                                      "ncu's FP64 pipe-active fraction is the issue-rate bound",
-                         "kernel_share_of_step": cg_ms / ms},
+                         "kernel_share_of_step": cg_ms / ms,
+                         "hbm_effective": {"achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                                           "frac": achieved / hbm_peak, "peak_kind": peak_kind,
+                                           "bytes_model": "352 B/site/CG-iteration (SURVEY 8(d) "
+                                                          "streaming model)",
+                                           "algorithmic_bytes_per_launch":
+                                               cg_bytes / max(1, n_solves),
+                                           "note": "a streaming-model rate, not a roofline "
+                                                   "fraction: the solve does not stream HBM"}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
@@ -1093,8 +1130,35 @@ def run_cfg5(args):
     return 0
 
 
+def _free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def launch_ranks(n):
+    """`python bench.py --gpus N` outside torchrun: start the N ranks (one
+    process per GPU) under torch.distributed.run on this node and return its
+    exit code.  The ranks see WORLD_SIZE = N and run the same arguments."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and args.gpus > 1:
+        return launch_ranks(args.gpus)
+    if world is not None and int(world) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one rank per GPU "
+              "(torchrun --nproc-per-node N bench.py --gpus N) or drop the launcher",
+              file=sys.stderr)
+        return 2
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "cfg5":

@@ -86,6 +86,7 @@ class StripLattice:
         if transport == "local" and multi:
             raise ValueError("the local transport keeps every strip in one process")
         self.transport = transport
+        self.group = group   # every collective of this lattice runs on it (None: the default group)
         if multi:
             self.world = dist.get_world_size(group)
             self.rank = dist.get_rank(group)

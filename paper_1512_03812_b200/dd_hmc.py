@@ -290,26 +290,27 @@ def _run_program(st: DDState, scheme: str, h: float, m: int, fgc: float):
             raise NotImplementedError(f"{name} in {scheme} is not wired for strips")
 
 
-def _global_sum(lat: StripLattice, per_strip: torch.Tensor) -> float:
-    v = per_strip.sum() if lat.S > 1 else per_strip[0]
+def _global_sums(lat: StripLattice, per_strip: torch.Tensor) -> list[float]:
+    """Whole-lattice sums of the per-strip values (K, S): strips added in
+    strip order, then across the lattice's ranks (lat.group) — one
+    collective and one host read for all K sums."""
+    v = per_strip[:, 0].clone()
+    for s in range(1, lat.S):
+        v = v + per_strip[:, s]
     if lat.world > 1:
-        v = v.clone()
-        dist.all_reduce(v)
-    return float(v.item())
+        dist.all_reduce(v, group=lat.group)
+    return v.tolist()
 
 
 def dd_hamiltonian(st: DDState) -> float:
     """H = kin + S_G + S_F over the whole lattice (hmc.py:44-51)."""
-    def own(kind, a, b=None):
-        out = torch.empty((st.S,), dtype=torch.float64, device=st.q.device)
-        _call("sch_dd_own_sum", st.lat._handle, kind, _lib.ptr(a), _lib.ptr(b), _lib.ptr(out))
-        return _global_sum(st.lat, out)
-
-    kin = own(0, st.p)
-    s_g = st.beta * own(1, st.q)
     _, _, xi = st.solve_pair()
-    s_f = own(2, st.eta, xi)
-    return (kin + s_g) + s_f
+    out = torch.empty((3, st.S), dtype=torch.float64, device=st.q.device)
+    _call("sch_dd_own_sum", st.lat._handle, 0, _lib.ptr(st.p), None, _lib.ptr(out[0]))
+    _call("sch_dd_own_sum", st.lat._handle, 1, _lib.ptr(st.q), None, _lib.ptr(out[1]))
+    _call("sch_dd_own_sum", st.lat._handle, 2, _lib.ptr(st.eta), _lib.ptr(xi), _lib.ptr(out[2]))
+    kin, gsum, s_f = _global_sums(st.lat, out)
+    return (kin + st.beta * gsum) + s_f
 
 
 def dd_integrate(st: DDState, spec: IntegratorSpec, tau: float):

@@ -3,15 +3,18 @@ do not need the oracle to redo the whole run:
 
 * cfg2 (4096 x 32^2): every batch element of the fused D^dag D against the
   oracle's batched NumPy stencil; linearity and hermiticity of D^dag D over
-  the whole batch; CG to 1e-10 in both stop modes with the true residual of
-  every chain recomputed by the oracle, and sampled chains' iteration
-  counts equal to the oracle's unbatched solve.
+  the whole batch; the per-chain CG to 1e-10: every one of the 4096
+  solutions against the oracle's per-chain solve (<= 1e-12 relative per
+  chain) with identical iteration counts for every chain (the oracle spread
+  over the host cores, oracle/parallel.py); the batch-global CG with every
+  chain's true residual recomputed by the oracle.
 * cfg3 (8192 x 16^2): one HMC update of the whole ensemble on the
-  reference's own per-chain streams; sampled chains equal independent
-  oracle hmc_update calls (dH <= 1e-8, accept, links); every chain's dH is
-  finite and the acceptance is the schedule's.
-* cfg4 (1024 x 64^2, m0 = 0.02): per-chain CG (cluster engine) with every
-  chain's true residual recomputed by the oracle; sampled iteration counts.
+  reference's own per-chain streams; 512 chains spread over the ensemble
+  equal independent oracle hmc_update calls (dH <= 1e-8, accept, links,
+  inversions); every chain's dH is finite and the acceptance is the
+  schedule's.
+* cfg4 (1024 x 64^2, m0 = 0.02): per-chain CG (cluster engine): every
+  chain's solution (<= 1e-12) and iteration count against the oracle.
 * cfg5 (2048^2): the decomposed D^dag D (local and peer-memory transports)
   against the oracle on the whole lattice, and the decomposed CG's true
   residual.
@@ -84,21 +87,30 @@ def test_cfg2_ddagd_linear_and_hermitian_over_the_batch(cfg2):
     assert float((xax.imag.abs() / xax.real).max()) < 1e-12 and bool((xax.real > 0).all())
 
 
-@pytest.mark.parametrize("stop", ["per_chain", "batch_global"])
-def test_cfg2_cg_true_residual_of_every_chain(cfg2, stop):
+def test_cfg2_cg_every_chain_equals_oracle(cfg2):
+    """All 4096 per-chain solves: solution <= 1e-12 relative per chain and the
+    same iteration count as the oracle's per-chain CG (fermion.py:171-217)."""
+    import paper_1512_03812_b200 as sw
+    from oracle import parallel as OP
+    q, psi = cfg2
+    op = sw.WilsonDirac(q, 0.1)
+    x, iters, rel = sw.cg_normal(op, psi, 1e-10, stop="per_chain")
+    xo, ito = OP.cg_per_chain(q, psi, 0.1, 1e-10)
+    its = np.asarray(iters)
+    assert its.shape == (4096,) and np.array_equal(its, ito), np.flatnonzero(its != ito)[:8]
+    err = per_element_rel(npy(x), xo)
+    assert err.max() < TOL_OP, (err.argmax(), err.max())
+
+
+def test_cfg2_batch_global_cg_true_residual_of_every_chain(cfg2):
     import paper_1512_03812_b200 as sw
     from oracle import schwinger_oracle as O
     q, psi = cfg2
     op = sw.WilsonDirac(q, 0.1)
-    x, iters, rel = sw.cg_normal(op, psi, 1e-10, stop=stop)
+    x, iters, rel = sw.cg_normal(op, psi, 1e-10, stop="batch_global")
     U = O.fermion_links(q)
     rr = true_relres(O, U, 0.1, npy(x), psi)
     assert rr.max() <= 1.0001e-10, rr.max()
-    if stop == "per_chain":
-        its = np.asarray(iters)
-        for c in np.random.default_rng(0).choice(4096, 6, replace=False):
-            _, ito, _ = O.cg_normal(U[c], 0.1, psi[c], 1e-10)
-            assert int(its[c]) == int(ito), c
 
 
 def test_cfg3_full_ensemble_update_matches_reference_chains():
@@ -116,18 +128,25 @@ def test_cfg3_full_ensemble_update_matches_reference_chains():
     # every chain finished with a finite energy change; from a hot start the
     # 4-step schedule accepts ~0.97 of the chains (3 -> 0.86, 5 -> 0.99)
     assert np.isfinite(st.dh).all() and st.accepted.mean() > 0.9
-    for c in (0, 1, 4095, 8191):
-        rng = O.make_rng(2024, c)
-        qc = O.hot_start(rng, L, L)
-        assert np.array_equal(qc, npy(q0[c]))
-        qo, so = O.hmc_update(qc, ocfg, rng)
-        assert abs(st.dh[c] - so["dh"]) < 1e-8, c
-        assert bool(st.accepted[c]) == so["accepted"], c
+    from oracle import parallel as OP
+    chains = sorted(set(range(0, B, 16)) | {1, 4095, 8191})   # 515 chains over the ensemble
+    ref = OP.hmc_chains(chains, 2024, kw, n_traj=1)
+    q0n = npy(q0)
+    for c in chains:
+        qs, qo, dh, acc, inv = ref[c]
+        assert np.array_equal(qs, q0n[c]), c
+        assert abs(st.dh[c] - dh[0]) < 1e-8, c
+        assert bool(st.accepted[c]) == bool(acc[0]), c
         assert np.max(np.abs(q1[c] - qo)) < 1e-8, c
+    assert int(st.inversions) == int(ref[0][4][0])
 
 
-def test_cfg4_cluster_cg_true_residual_of_every_chain():
+def test_cfg4_cluster_cg_every_chain_equals_oracle():
+    """All 1024 per-chain 64^2 solves (cluster engine) against the oracle's
+    per-chain CG: identical iteration counts, solutions <= 1e-12 per chain,
+    and every chain's true residual recomputed by the oracle."""
     import paper_1512_03812_b200 as sw
+    from oracle import parallel as OP
     from oracle import schwinger_oracle as O
     rng = np.random.default_rng(1024)
     B, L, m0 = 1024, 64, 0.02
@@ -135,13 +154,14 @@ def test_cfg4_cluster_cg_true_residual_of_every_chain():
     b = rng.standard_normal((B, L, L, 2)) + 1j * rng.standard_normal((B, L, L, 2))
     op = sw.WilsonDirac(q, m0)
     x, iters, _ = sw.cg_normal(op, b, 1e-10, stop="per_chain")
-    U = O.fermion_links(q)
-    rr = true_relres(O, U, m0, npy(x), b)
+    x = npy(x)
+    rr = true_relres(O, O.fermion_links(q), m0, x, b)
     assert rr.max() <= 1.0001e-10, rr.max()
+    xo, ito = OP.cg_per_chain(q, b, m0, 1e-10)
     its = np.asarray(iters)
-    for c in (0, 777):
-        _, ito, _ = O.cg_normal(U[c], m0, b[c], 1e-10)
-        assert int(its[c]) == int(ito), c
+    assert np.array_equal(its, ito), np.flatnonzero(its != ito)[:8]
+    err = per_element_rel(x, xo)
+    assert err.max() < TOL_OP, (err.argmax(), err.max())
 
 
 @pytest.mark.parametrize("transport", ["local", "p2p"])

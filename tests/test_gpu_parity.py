@@ -227,13 +227,15 @@ def test_forces_match_reference(sw, golden, tag):
     b1, b2 = F.weighted_w_sums(op, g[f"{tag}_f"], g[f"{tag}_chi"], g[f"{tag}_xi"])
     assert rel_err(npy(b1), g[f"{tag}_b1"]) < TOL_OP
     assert rel_err(npy(b2), g[f"{tag}_b2"]) < TOL_OP
+    # the Z pair and the FG contractions at the north_star bar (measured on B200,
+    # tools/parity_errors.py: <= 2.4e-13 for every piece of both cases)
     z1, z2 = F.z_pair(op, g[f"{tag}_f"], g[f"{tag}_chi"], g[f"{tag}_xi"], tol)
-    assert rel_err(npy(z1), g[f"{tag}_z1"]) < 1e-11
-    assert rel_err(npy(z2), g[f"{tag}_z2"]) < 1e-11
+    assert rel_err(npy(z1), g[f"{tag}_z1"]) < TOL_OP
+    assert rel_err(npy(z2), g[f"{tag}_z2"]) < TOL_OP
     fgff = F.fg_fermion_hessian_dot(op, g[f"{tag}_chi"], g[f"{tag}_xi"], g[f"{tag}_f"], tol)
-    assert rel_err(npy(fgff), g[f"{tag}_fgff"]) < 1e-11
+    assert rel_err(npy(fgff), g[f"{tag}_fgff"]) < TOL_OP
     fggf = F.fg_fermion_hessian_dot(op, g[f"{tag}_chi"], g[f"{tag}_xi"], g[f"{tag}_g"], tol)
-    assert rel_err(npy(fggf), g[f"{tag}_fggf"]) < 1e-11
+    assert rel_err(npy(fggf), g[f"{tag}_fggf"]) < TOL_OP
     assert rel_err(npy(sw.gauge_force(q, beta)), g[f"{tag}_g"]) < 1e-14
     from paper_1512_03812_b200 import gauge as G
     assert np.array_equal(npy(G.plaq_angles(q)), g[f"{tag}_plaq"])
