@@ -221,8 +221,11 @@ int sch_dd_p2p_connect(sch_ctx* ctx, sch_dd* dd, const void* ipc_handles);
 int sch_dd_geometry(const sch_dd* dd, int* out4);
 /* refresh the halo rows of a field [S][planes][Lext][T][words_per_site] (doubles) */
 int sch_dd_exchange(sch_ctx* ctx, sch_dd* dd, double* field, int planes, int words_per_site);
-/* out[s] = per-strip sum over the own rows: kind 0 = 0.5*sum p^2 (momenta),
- * 1 = sum(1 - cos theta) (links), 2 = Re sum conj(a) b (spinors a, b) */
+/* *out (device) = whole-lattice sum over every strip's own rows, formed by
+ * the canonical tree through the lattice's transport (the same bits on
+ * every rank, for any strip count): kind 0 = sum p^2 (momenta; the caller
+ * takes 0.5x, lattice.py:128-130), 1 = sum(1 - cos theta) (links,
+ * gauge.py:37-40), 2 = Re sum conj(a) b (spinors a, b, fermion.py:54-56) */
 int sch_dd_own_sum(sch_ctx* ctx, sch_dd* dd, int kind, const double* a, const double* b,
                    double* out);
 /* out = D^dag D psi on the own rows (psi's halos are refreshed first);

@@ -137,6 +137,16 @@ SCH_DEV double warp_sum(double v) {
   return v;
 }
 
+// Canonical tree sum over the 32 lanes (lane l holds value l): a balanced
+// binary tree in index order, adjacent pairs first (xor 1, 2, ..., 16);
+// every lane ends with the same value.  Zero padding a shorter sequence to
+// 32 lanes leaves this tree's value unchanged.
+SCH_DEV double warp_tree_sum(double v) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 template <int NT>
 SCH_DEV double block_sum(double v, double* slot) {
   constexpr int NW = NT / 32;

@@ -59,7 +59,6 @@ namespace {
 
 constexpr int kHalo = 2;
 constexpr int kDDReplace = 50;
-constexpr int kRedGrid = 296;   // fixed grid of the elementwise passes (deterministic partials)
 
 // ---------------------------------------------------------------- NCCL (dlopen)
 struct NcclApi {
@@ -72,6 +71,8 @@ struct NcclApi {
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
@@ -93,9 +94,10 @@ NcclApi& nccl() {
       api.Send = (decltype(api.Send))sym("ncclSend");
       api.Recv = (decltype(api.Recv))sym("ncclRecv");
       api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+      api.AllGather = (decltype(api.AllGather))sym("ncclAllGather");
       api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
       api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart &&
-               api.GroupEnd && api.Send && api.Recv && api.AllReduce;
+               api.GroupEnd && api.Send && api.Recv && api.AllReduce && api.AllGather;
     }
   }
   return api;
@@ -127,6 +129,12 @@ struct sch_dd {
   // finished in the current exchange.  Kept on the device so the kernels
   // find their sequence number themselves and a CG loop can be captured.
   unsigned long long* seq_dev = nullptr;
+  // canonical global sums (see "Decomposition-invariant sums" below)
+  int CW = 0, NC = 0;                 // row-chunk width and chunks per row (T / CW)
+  int* red_ctr = nullptr;             // last-CTA ticket of k_dd_rowred (self-resetting)
+  double* red_blk = nullptr;          // [S][nb] 64-row block values
+  double* red_all = nullptr;          // [0]: this rank's strip value, [1..G]: all-gathered (NCCL)
+  double* own_part = nullptr;         // [S][Lloc][NC] row partials of sch_dd_own_sum
 };
 
 namespace {
@@ -261,7 +269,6 @@ __global__ void k_dd_exchange_local(double* __restrict__ f, int S, int P, int Le
 }
 
 int p2p_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W);
-int p2p_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out, const DDPost& post);
 
 int dd_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
   if (dd->p2p) return p2p_exchange(ctx, dd, f, P, W);
@@ -288,37 +295,6 @@ int dd_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
     SCH_NCCL(ctx, n.Recv(base + (dd->Lloc + 2) * row, face, ncclDouble, right, dd->comm, ctx->stream));
   }
   SCH_NCCL(ctx, n.GroupEnd());
-  return SCH_OK;
-}
-
-// global sum of the S*n partials (fixed order) into *out, then across ranks
-__global__ void k_dd_sum(const double* __restrict__ part, int n, double* __restrict__ out, DDPost post) {
-  __shared__ double slot[32];
-  double acc = 0.0;
-  for (int k = threadIdx.x; k < n; k += blockDim.x) acc += part[k];
-  double s = block_sum_rt(acc, slot);
-  if (threadIdx.x == 0) {
-    *out = s;
-    dd_post_run(post);
-  }
-}
-
-// part holds n partials per local strip, [S][n]
-// part holds n partials per local strip, [S][n]; `post` runs on the sum
-int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out,
-              const DDPost& post = DDPost{}) {
-  if (dd->p2p) return p2p_allsum(ctx, dd, part, n, out, post);
-  if (dd->comm == nullptr && dd->nranks > 1)
-    return sch_fail(ctx, SCH_ERR_ARG, "dd: no transport (NCCL id or p2p connect)");
-  k_dd_sum<<<1, 256, 0, ctx->stream>>>(part, dd->S * n, out, dd->comm ? DDPost{} : post);
-  SCH_LAUNCHED(ctx);
-  if (dd->comm != nullptr) {
-    SCH_NCCL(ctx, nccl().AllReduce(out, out, 1, ncclDouble, ncclSum, dd->comm, ctx->stream));
-    if (post.kind != POST_NONE) {
-      k_dd_post<<<1, 1, 0, ctx->stream>>>(post);
-      SCH_LAUNCHED(ctx);
-    }
-  }
   return SCH_OK;
 }
 
@@ -440,33 +416,35 @@ __global__ void k_p2p_pull(double* __restrict__ f, int P, int W, P2PArgs a) {
   }
 }
 
-// one CTA per local strip: the strip's partials (fixed order) -> slot
-// [seq parity][g] of every mailbox, then its flag [g] = seq (release)
-__global__ void k_p2p_red_push(const double* __restrict__ part, int n, P2PArgs a) {
-  __shared__ double slot[32];
-  const unsigned long long seq = *(volatile unsigned long long*)(a.seq + 1) + 1;
-  const int s = blockIdx.x, g = a.strip0 + s;
-  double acc = 0.0;
-  for (int k = threadIdx.x; k < n; k += blockDim.x) acc += part[(long long)s * n + k];
-  const double v = block_sum_rt(acc, slot);
-  if (threadIdx.x == 0) {
-    for (int h = 0; h < a.G; ++h) ((double*)(a.tab[h] + a.off_red))[(seq % kNBuf) * a.G + g] = v;
-    __threadfence_system();
-    for (int h = 0; h < a.G; ++h) st_release_sys(box_u64(a, h, a.off_redflag) + g, seq);
+// Canonical tree (balanced, index order, zero padded) of n <= 256 values in
+// global memory by one warp: lane l owns [l*K, l*K + K), K = the power of two
+// >= n/32; every lane returns the sum.
+SCH_DEV double warp_canon(const double* v, int n, int lane) {
+  int K = 1;
+  while (32 * K < n) K <<= 1;
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const int i = lane * K + k;
+    a[k] = (k < K && i < n) ? __ldcg(v + i) : 0.0;
   }
+#pragma unroll
+  for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+    for (int k = 0; k < w; ++k) a[k] = a[2 * k] + a[2 * k + 1];
+  return warp_tree_sum(a[0]);
 }
 
-// wait for the G contributions of sum `seq` in the first local strip's
-// mailbox, add them in strip order (the same bits on every rank)
+// wait for the G strip values of sum `seq` in the first local strip's
+// mailbox and combine them by the canonical tree (the same bits on every rank)
 __global__ void k_p2p_red_finish(P2PArgs a, double* __restrict__ out, DDPost post) {
   const int g0 = a.strip0;
   const unsigned long long seq = *(volatile unsigned long long*)(a.seq + 1) + 1;
   for (int h = threadIdx.x; h < a.G; h += blockDim.x) spin_until(box_u64(a, g0, a.off_redflag) + h, seq);
   __syncwarp();
+  const double* red = (const double*)(a.tab[g0] + a.off_red) + (seq % kNBuf) * a.G;
+  const double v = warp_canon(red, a.G, threadIdx.x & 31);
   if (threadIdx.x == 0) {
-    const double* red = (const double*)(a.tab[g0] + a.off_red) + (seq % kNBuf) * a.G;
-    double v = 0.0;
-    for (int h = 0; h < a.G; ++h) v += __ldcg(red + h);
     *out = v;
     dd_post_run(post);
   }
@@ -502,37 +480,198 @@ int p2p_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
   return SCH_OK;
 }
 
-int p2p_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, int n, double* out, const DDPost& post) {
-  const P2PArgs a = p2p_args(dd);
-  k_p2p_red_push<<<dd->S, 256, 0, ctx->stream>>>(part, n, a);
-  k_p2p_red_finish<<<1, 32, 0, ctx->stream>>>(a, out, post);
-  ctx->launches += 2;
+// ------------------------------------------ decomposition-invariant sums
+// Every global sum of the decomposed lattice (the CG's <p,Ap>, ||r||^2,
+// ||b - Ax||^2, ||b||^2 and the Hamiltonian's terms) is one fixed
+// expression of its site values:
+//     sum = C_x ( C_c ( C_t (site value) ) )
+// C is the canonical tree — a balanced binary tree over the values in index
+// order, zero padded to a power of two; x runs over the L global rows, c
+// over the T/CW chunks of a row, t over the CW sites of a chunk.  The
+// producing kernels write one partial per (own row, chunk) (row_chunk_sum,
+// tile.cuh, and the warp-per-chunk passes below); k_dd_rowred forms each
+// strip's value, C over its rows (64-row blocks, then the blocks), and the
+// strips' values are combined by C over the G strips: inside the kernel for
+// the local transport, by k_p2p_red_finish after the mailbox pushes, or by
+// k_dd_tree_post after an ncclAllGather of the G values.  With a power-of-
+// two strip height Lloc every strip is a subtree of C over the L rows, so
+// each sum — and with it every CG iteration count, stopping decision and
+// Hamiltonian — is bit-identical for every number of strips G and every
+// transport.
+enum { RED_LOCAL = 0, RED_P2P = 1, RED_NCCL = 2 };
+constexpr int kRowBlk = 64;     // rows per CTA of k_dd_rowred
+constexpr int kMaxCanon = 1024; // values one CTA combines (blocks per strip, strips)
+
+struct RowRed {
+  const double* part;   // [S][Lloc][nch] row-chunk partials
+  int S, Lloc, nch, nb; // nb = ceil(Lloc / kRowBlk)
+  double* blk;          // [S][nb]
+  int* ctr;             // last-CTA ticket (reset by the last CTA)
+  int mode;
+  double* out;          // local: the global sum; NCCL: this rank's strip value
+  DDPost post;          // local transport: the CG control fused into the sum
+  P2PArgs pa;           // p2p transport: mailboxes
+};
+
+// C over n <= kMaxCanon values (global when GLOBAL, else shared), by the
+// whole CTA, ping-pong through two shared buffers; every thread returns it
+template <bool GLOBAL>
+SCH_DEV double block_canon(const double* v, int n, double* t0, double* t1) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = threadIdx.x; i < P; i += blockDim.x)
+    t0[i] = i < n ? (GLOBAL ? __ldcg(v + i) : v[i]) : 0.0;
+  __syncthreads();
+  for (int w = P >> 1; w >= 1; w >>= 1) {
+    for (int i = threadIdx.x; i < w; i += blockDim.x) t1[i] = t0[2 * i] + t0[2 * i + 1];
+    __syncthreads();
+    double* tmp = t0;
+    t0 = t1;
+    t1 = tmp;
+  }
+  const double r = t0[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) k_dd_rowred(RowRed a) {
+  __shared__ double rv[kRowBlk];
+  __shared__ double t0[kMaxCanon], t1[kMaxCanon], sv[kMaxCanon];
+  __shared__ int last;
+  const int b = blockIdx.x, s = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int RPW = kRowBlk / 8;   // rows per warp (8 warps)
+  for (int i = 0; i < RPW; ++i) {
+    const int y = b * kRowBlk + warp * RPW + i;
+    double v = 0.0;
+    if (y < a.Lloc) v = warp_canon(a.part + ((long long)s * a.Lloc + y) * a.nch, a.nch, lane);
+    if (lane == 0) rv[warp * RPW + i] = v;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const double v = warp_tree_sum(rv[2 * lane] + rv[2 * lane + 1]);
+    if (lane == 0) {
+      a.blk[(long long)s * a.nb + b] = v;
+      __threadfence();
+      last = atomicAdd(a.ctr, 1) == a.nb * a.S - 1;
+    }
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int st = 0; st < a.S; ++st) {
+    const double v = block_canon<true>(a.blk + (long long)st * a.nb, a.nb, t0, t1);
+    if (threadIdx.x == 0) sv[st] = v;
+  }
+  __syncthreads();
+  if (a.mode == RED_LOCAL) {
+    const double v = block_canon<false>(sv, a.S, t0, t1);
+    if (threadIdx.x == 0) {
+      *a.out = v;
+      dd_post_run(a.post);
+    }
+  } else if (a.mode == RED_NCCL) {
+    if (threadIdx.x == 0) *a.out = sv[0];
+  } else if (threadIdx.x == 0) {   // p2p: strip values -> slot [seq parity][g] of every mailbox
+    const P2PArgs& pa = a.pa;
+    const unsigned long long seq = *(volatile unsigned long long*)(pa.seq + 1) + 1;
+    for (int st = 0; st < a.S; ++st) {
+      const int g = pa.strip0 + st;
+      for (int h = 0; h < pa.G; ++h) ((double*)(pa.tab[h] + pa.off_red))[(seq % kNBuf) * pa.G + g] = sv[st];
+    }
+    __threadfence_system();
+    for (int st = 0; st < a.S; ++st)
+      for (int h = 0; h < pa.G; ++h) st_release_sys(box_u64(pa, h, pa.off_redflag) + pa.strip0 + st, seq);
+  }
+  if (threadIdx.x == 0) *a.ctr = 0;
+}
+
+// NCCL transport: C over the G all-gathered strip values
+__global__ void k_dd_tree_post(const double* __restrict__ vals, int G, double* __restrict__ out,
+                               DDPost post) {
+  const double v = warp_canon(vals, G, threadIdx.x & 31);
+  if (threadIdx.x == 0) {
+    *out = v;
+    dd_post_run(post);
+  }
+}
+
+// the global sum of the row partials `part` ([S][Lloc][NC]) into *out (on
+// the device, every rank); `post` runs on the sum
+int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, double* out,
+              const DDPost& post = DDPost{}) {
+  if (!dd->p2p && dd->comm == nullptr && dd->nranks > 1)
+    return sch_fail(ctx, SCH_ERR_ARG, "dd: no transport (NCCL id or p2p connect)");
+  RowRed a;
+  a.part = part;
+  a.S = dd->S;
+  a.Lloc = dd->Lloc;
+  a.nch = dd->NC;
+  a.nb = (dd->Lloc + kRowBlk - 1) / kRowBlk;
+  a.blk = dd->red_blk;
+  a.ctr = dd->red_ctr;
+  a.mode = dd->p2p ? RED_P2P : dd->comm ? RED_NCCL : RED_LOCAL;
+  a.out = a.mode == RED_NCCL ? dd->red_all : out;
+  a.post = a.mode == RED_LOCAL ? post : DDPost{};
+  a.pa = dd->p2p ? p2p_args(dd) : P2PArgs{};
+  k_dd_rowred<<<dim3(a.nb, dd->S), 256, 0, ctx->stream>>>(a);
+  SCH_LAUNCHED(ctx);
+  if (a.mode == RED_P2P) {
+    k_p2p_red_finish<<<1, 32, 0, ctx->stream>>>(a.pa, out, post);
+    SCH_LAUNCHED(ctx);
+  } else if (a.mode == RED_NCCL) {
+    SCH_NCCL(ctx, nccl().AllGather(dd->red_all, dd->red_all + 1, 1, ncclDouble, dd->comm, ctx->stream));
+    k_dd_tree_post<<<1, 32, 0, ctx->stream>>>(dd->red_all + 1, dd->G, out, post);
+    SCH_LAUNCHED(ctx);
+  }
   return SCH_OK;
 }
 
-// x = x0|0 (all rows), r = p = b (all rows; b halos already exchanged),
-// partial ||b||^2 over own rows
+// Warp-per-chunk passes: a work item is (strip s, extended row xr, chunk ch);
+// lane l owns sites ch*CW + l*K + k (k < K; K = 2 for CW = 64, else 1 and
+// lanes >= CW idle), and an own row's chunk partial is C over its CW site
+// values — the same tree as row_chunk_sum in the tile kernels.
+struct ChunkItem {
+  int s, xr, ch;
+};
+SCH_DEV ChunkItem chunk_item(long long w, int nch, int rows) {
+  ChunkItem c;
+  c.ch = (int)(w % nch);
+  const long long sr = w / nch;
+  c.xr = (int)(sr % rows);
+  c.s = (int)(sr / rows);
+  return c;
+}
+
+// x = x0|0, r = p = b on every row (b's halos already exchanged); the row
+// partials of ||b||^2 on the own rows
 __global__ void k_dd_init(const double2* __restrict__ b, const double2* __restrict__ x0,
                           double2* __restrict__ x, double2* __restrict__ r, double2* __restrict__ p,
-                          long long nsites, int T, int Lext, int lo, int hi, double* __restrict__ part) {
-  // grid (gx, S): strip blockIdx.y, partial [strip][blockIdx.x]
-  __shared__ double slot[32];
-  double acc = 0.0;
-  const long long ns = (long long)Lext * T, s0 = blockIdx.y * ns;
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < ns;
-       k += (long long)gridDim.x * blockDim.x) {
-    const long long i = s0 + k;
-    Spinor bv = ld256_spinor_nc(b, i);
-    Spinor xv;
-    if (x0) xv = ld256_spinor_nc(x0, i);
-    else xv.s0 = xv.s1 = make_double2(0, 0);
-    st256_spinor(x, i, xv);
-    st256_spinor(r, i, bv);
-    st256_spinor(p, i, bv);
-    if (own_row(k, T, Lext, lo, hi)) acc += spinor_norm2(bv);
+                          int S, int Lext, int T, int CW, int lo, int hi, double* __restrict__ rowpart) {
+  const int lane = threadIdx.x & 31, K = CW > 32 ? 2 : 1, nch = T / CW;
+  const long long items = (long long)S * Lext * nch;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nw) {
+    const ChunkItem c = chunk_item(w, nch, Lext);
+    double v[2] = {0.0, 0.0};
+    for (int k = 0; k < K; ++k) {
+      const int j = lane * K + k;
+      if (j >= CW) continue;
+      const long long i = ((long long)c.s * Lext + c.xr) * T + c.ch * CW + j;
+      Spinor bv = ld256_spinor_nc(b, i);
+      Spinor xv;
+      if (x0) xv = ld256_spinor_nc(x0, i);
+      else xv.s0 = xv.s1 = make_double2(0, 0);
+      st256_spinor(x, i, xv);
+      st256_spinor(r, i, bv);
+      st256_spinor(p, i, bv);
+      v[k] = spinor_norm2(bv);
+    }
+    if (c.xr >= lo && c.xr < hi) {   // warp-uniform
+      const double t = warp_tree_sum(v[0] + v[1]);
+      if (lane == 0) rowpart[((long long)c.s * (hi - lo) + (c.xr - lo)) * nch + c.ch] = t;
+    }
   }
-  double s = block_sum_rt(acc, slot);
-  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = s;
 }
 
 __global__ void k_dd_copy(const double2* __restrict__ src, double2* __restrict__ dst, long long nsites) {
@@ -559,79 +698,82 @@ __global__ void k_dd_ctrl_init(DDState st, int S, double tol, int have_x0) {
   st.ctl[3] = 1;
 }
 
-// p = r + beta p, x += alpha p on every row; r -= alpha ap and ||r||^2 on own rows
+// p = r + beta p, x += alpha p on every row; r -= alpha ap and the row
+// partials of ||r||^2 on the own rows (not on residual-replacement
+// iterations, where the true-residual pass forms r)
 __global__ void k_dd_update(double2* __restrict__ r, double2* __restrict__ p, double2* __restrict__ x,
-                            const double2* __restrict__ ap, DDState st, long long nsites, int T, int Lext,
-                            int lo, int hi, double* __restrict__ part) {
-  __shared__ double slot[32];
+                            const double2* __restrict__ ap, DDState st, int S, int Lext, int T, int CW,
+                            int lo, int hi, double* __restrict__ rowpart) {
   if (st.ctl[0]) return;
   const int repl = (st.ctl[3] % kDDReplace) == 0;
   const double al = st.sc[SC_ALPHA], be = st.beta[0];
-  double acc = 0.0;
-  const long long ns = (long long)Lext * T, s0 = blockIdx.y * ns;   // grid (gx, S) as k_dd_init
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < ns;
-       k += (long long)gridDim.x * blockDim.x) {
-    const long long i = s0 + k;
-    Spinor rv = ld256_spinor(r, i), pv = ld256_spinor(p, i), xv = ld256_spinor(x, i);
-    pv = sp_fma(be, pv, rv);
-    xv = sp_fma(al, pv, xv);
-    st256_spinor(p, i, pv);
-    st256_spinor(x, i, xv);
-    if (!repl && own_row(k, T, Lext, lo, hi)) {
-      rv = sp_fma(-al, ld256_spinor_nc(ap, i), rv);
-      st256_spinor(r, i, rv);
-      acc += spinor_norm2(rv);
+  const int lane = threadIdx.x & 31, K = CW > 32 ? 2 : 1, nch = T / CW;
+  const long long items = (long long)S * Lext * nch;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nw) {
+    const ChunkItem c = chunk_item(w, nch, Lext);
+    const bool own = c.xr >= lo && c.xr < hi;
+    double v[2] = {0.0, 0.0};
+    for (int k = 0; k < K; ++k) {
+      const int j = lane * K + k;
+      if (j >= CW) continue;
+      const long long i = ((long long)c.s * Lext + c.xr) * T + c.ch * CW + j;
+      Spinor rv = ld256_spinor(r, i), pv = ld256_spinor(p, i), xv = ld256_spinor(x, i);
+      pv = sp_fma(be, pv, rv);
+      xv = sp_fma(al, pv, xv);
+      st256_spinor(p, i, pv);
+      st256_spinor(x, i, xv);
+      if (!repl && own) {
+        rv = sp_fma(-al, ld256_spinor_nc(ap, i), rv);
+        st256_spinor(r, i, rv);
+        v[k] = spinor_norm2(rv);
+      }
+    }
+    if (own) {
+      const double t = warp_tree_sum(v[0] + v[1]);
+      if (lane == 0) rowpart[((long long)c.s * (hi - lo) + (c.xr - lo)) * nch + c.ch] = t;
     }
   }
-  double s = block_sum_rt(acc, slot);
-  if (threadIdx.x == 0) part[blockIdx.y * gridDim.x + blockIdx.x] = s;
 }
 
-TileShape dd_tiles(int Lext, int T) { return pick_tile(Lext, T, false); }
-
-// own-row sums, one CTA column per strip, fixed grid => deterministic
+// Row partials of the Hamiltonian's sums over the own rows (site values:
+// kind 0 p_0^2 + p_1^2, kind 1 1 - cos theta, kind 2 Re conj(a) b over the
+// two spin components)
 __global__ void k_dd_own_sum(int kind, const double* __restrict__ a, const double* __restrict__ b,
-                             int Lext, int T, int lo, int hi, double* __restrict__ part) {
-  __shared__ double slot[32];
-  const int s = blockIdx.y;
+                             int S, int Lext, int T, int CW, int lo, int hi,
+                             double* __restrict__ rowpart) {
+  const int lane = threadIdx.x & 31, K = CW > 32 ? 2 : 1, nch = T / CW, own = hi - lo;
   const long long plane = (long long)Lext * T;
-  const long long own = (long long)(hi - lo) * T;
-  double acc = 0.0;
-  if (kind == 0) {
-    const double* ps = a + (long long)s * 2 * plane;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 2 * own;
-         i += (long long)gridDim.x * blockDim.x) {
-      const long long mu = i / own, k = i - mu * own;
-      const double v = ps[mu * plane + lo * (long long)T + k];
-      acc += v * v;
+  const long long items = (long long)S * own * nch;
+  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nw) {
+    const ChunkItem c = chunk_item(w, nch, own);
+    const int x = lo + c.xr;
+    double v[2] = {0.0, 0.0};
+    for (int k = 0; k < K; ++k) {
+      const int j = lane * K + k;
+      if (j >= CW) continue;
+      const int t = c.ch * CW + j;
+      if (kind == 0) {
+        const double* ps = a + (long long)c.s * 2 * plane + (long long)x * T + t;
+        v[k] = ps[0] * ps[0] + ps[plane] * ps[plane];
+      } else if (kind == 1) {
+        v[k] = 1.0 - cos(plaq(a + (long long)c.s * 2 * plane, Lext, T, x, t));
+      } else {
+        const long long e = 2 * ((long long)c.s * plane + (long long)x * T + t);
+        const double2* as = (const double2*)a;
+        const double2* bs = (const double2*)b;
+        v[k] = redot(as[e], bs[e]) + redot(as[e + 1], bs[e + 1]);
+      }
     }
-  } else if (kind == 1) {
-    const double* qs = a + (long long)s * 2 * plane;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < own;
-         i += (long long)gridDim.x * blockDim.x) {
-      const int x = lo + (int)(i / T), t = (int)(i % T);
-      acc += 1.0 - cos(plaq(qs, Lext, T, x, t));
-    }
-  } else {
-    const double2* as = (const double2*)a + (long long)s * 2 * plane;
-    const double2* bs = (const double2*)b + (long long)s * 2 * plane;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 2 * own;
-         i += (long long)gridDim.x * blockDim.x) {
-      const long long e = 2 * lo * (long long)T + i;
-      acc += redot(as[e], bs[e]);
-    }
+    const double t = warp_tree_sum(v[0] + v[1]);
+    if (lane == 0) rowpart[((long long)c.s * own + c.xr) * nch + c.ch] = t;
   }
-  const double v = block_sum_rt(acc, slot);
-  if (threadIdx.x == 0) part[(long long)s * gridDim.x + blockIdx.x] = v;
 }
 
-__global__ void k_dd_strip_finish(const double* __restrict__ part, int S, int kind,
-                                  double* __restrict__ out) {
-  for (int s = threadIdx.x; s < S; s += blockDim.x) {
-    double v = 0.0;
-    for (int k = 0; k < kRedGrid; ++k) v += part[(long long)s * kRedGrid + k];
-    out[s] = kind == 0 ? 0.5 * v : v;
-  }
+// grid of the warp-per-chunk passes: enough warps for one wave
+inline unsigned chunk_grid(long long items) {
+  return (unsigned)std::max<long long>(1, std::min<long long>((items + 7) / 8, 148 * 8));
 }
 
 TileArgs dd_tile_args(sch_dd* dd, const TileShape& sh, const double2* U, double m0) {
@@ -677,6 +819,32 @@ int sch_dd_create(sch_ctx* ctx, const void* nccl_id, int nranks, int rank, int L
   dd->T = T;
   dd->Lloc = L / G;
   dd->Lext = dd->Lloc + 2 * kHalo;
+  TileShape sh;
+  if (dd_tile_shape(dd->Lext, T, sh)) {   // else: halo exchange only (stencils need T % 8 == 0)
+    dd->CW = sh.TT;
+    dd->NC = T / sh.TT;
+  } else {
+    dd->CW = 8;
+    dd->NC = 1;
+  }
+  {
+    const int nb = (dd->Lloc + kRowBlk - 1) / kRowBlk;
+    if (nb > kMaxCanon || dd->S > kMaxCanon || dd->NC > 256 || G > 256) {
+      delete dd;
+      return sch_fail(ctx, SCH_ERR_ARG, "dd_create: lattice too large for the canonical sums");
+    }
+    cudaError_t e = cudaMalloc(&dd->red_ctr, sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(dd->red_ctr, 0, sizeof(int));
+    if (e == cudaSuccess) e = cudaMalloc(&dd->red_blk, sizeof(double) * (size_t)nb * dd->S);
+    if (e == cudaSuccess) e = cudaMalloc(&dd->red_all, sizeof(double) * (G + 1));
+    if (e == cudaSuccess)
+      e = cudaMalloc(&dd->own_part, sizeof(double) * (size_t)dd->S * dd->Lloc * dd->NC);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+      sch_dd_destroy(dd);
+      return sch_fail(ctx, SCH_ERR_CUDA, "dd_create: %s", cudaGetErrorString(e));
+    }
+  }
   if (nranks > 1 && nccl_id != nullptr) {   // NCCL transport (else: p2p, connected later)
     if (!nccl().ok) {
       delete dd;
@@ -701,6 +869,10 @@ int sch_dd_destroy(sch_dd* dd) {
   if (dd->box_tab) cudaFree(dd->box_tab);
   if (dd->seq_dev) cudaFree(dd->seq_dev);
   if (dd->box_mem) cudaFree(dd->box_mem);
+  if (dd->red_ctr) cudaFree(dd->red_ctr);
+  if (dd->red_blk) cudaFree(dd->red_blk);
+  if (dd->red_all) cudaFree(dd->red_all);
+  if (dd->own_part) cudaFree(dd->own_part);
   delete dd;
   return SCH_OK;
 }
@@ -757,24 +929,22 @@ int sch_dd_geometry(const sch_dd* dd, int* out4) {
   return SCH_OK;
 }
 
-// Per-strip sums over the own rows of extended fields (the Hamiltonian's
-// reductions on a decomposed lattice):
-//   kind 0: 0.5 * sum a^2            a = momenta [S][2][Lext][T]      (lattice.py:128-130)
-//   kind 1: sum (1 - cos theta)      a = links   [S][2][Lext][T]      (gauge.py:37-40)
-//   kind 2: Re sum conj(a) b         a, b = spinors [S][Lext][T][2]   (fermion.py:54-56)
+// Whole-lattice sums over the own rows of extended fields (the
+// Hamiltonian's reductions on a decomposed lattice), through the canonical
+// tree and the lattice's transport, so every rank holds the same value:
+//   kind 0: sum p^2               a = momenta [S][2][Lext][T]      (lattice.py:128-130, x 0.5 by the caller)
+//   kind 1: sum (1 - cos theta)   a = links   [S][2][Lext][T]      (gauge.py:37-40)
+//   kind 2: Re sum conj(a) b      a, b = spinors [S][Lext][T][2]   (fermion.py:54-56)
 int sch_dd_own_sum(sch_ctx* ctx, sch_dd* dd, int kind, const double* a, const double* b,
                    double* out) {
   SCH_CHECK_ARG(ctx, dd && a && out && kind >= 0 && kind <= 2 && (kind != 2 || b),
                 "dd_own_sum: bad args");
-  void* ws;
-  int rc = sch_workspace(ctx, sizeof(double) * (size_t)dd->S * kRedGrid, &ws);
-  if (rc) return rc;
-  k_dd_own_sum<<<dim3(kRedGrid, dd->S), 256, 0, ctx->stream>>>(kind, a, b, dd->Lext, dd->T, kHalo,
-                                                               kHalo + dd->Lloc, (double*)ws);
+  SCH_CHECK_ARG(ctx, dd->T % 8 == 0, "dd_own_sum: T must be a multiple of 8");
+  const long long items = (long long)dd->S * dd->Lloc * dd->NC;
+  k_dd_own_sum<<<chunk_grid(items), 256, 0, ctx->stream>>>(kind, a, b, dd->S, dd->Lext, dd->T, dd->CW,
+                                                           kHalo, kHalo + dd->Lloc, dd->own_part);
   SCH_LAUNCHED(ctx);
-  k_dd_strip_finish<<<1, 64, 0, ctx->stream>>>((const double*)ws, dd->S, kind, out);
-  SCH_LAUNCHED(ctx);
-  return SCH_OK;
+  return dd_allsum(ctx, dd, dd->own_part, out);
 }
 
 int sch_dd_exchange(sch_ctx* ctx, sch_dd* dd, double* field, int planes, int words_per_site) {
@@ -785,13 +955,15 @@ int sch_dd_exchange(sch_ctx* ctx, sch_dd* dd, double* field, int planes, int wor
 int sch_dd_ddagd(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* psi_ext, double* out_ext,
                  double m0) {
   SCH_CHECK_ARG(ctx, dd && U_ext && psi_ext && out_ext && psi_ext != out_ext, "dd_ddagd: bad args");
+  SCH_CHECK_ARG(ctx, dd->T % 8 == 0, "dd_ddagd: T must be a multiple of 8");
   int rc = dd_exchange(ctx, dd, psi_ext, 1, 4);
   if (rc) return rc;
-  TileShape sh = dd_tiles(dd->Lext, dd->T);
+  TileShape sh;
+  dd_tile_shape(dd->Lext, dd->T, sh);
   TileArgs a = dd_tile_args(dd, sh, (const double2*)U_ext, m0);
   a.in = (const double2*)psi_ext;
   a.out = (double2*)out_ext;
-  launch_normal_tile<MODE_PLAIN>(sh, a, ctx->stream);
+  launch_dd_tile<MODE_PLAIN>(sh, a, ctx->stream);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
@@ -801,13 +973,13 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
                      double* h_relres, int* h_status) {
   SCH_CHECK_ARG(ctx, dd && U_ext && b_ext && x_ext && maxiter >= 1, "dd_cg_normal: bad args");
   SCH_CHECK_ARG(ctx, x_ext != b_ext && x_ext != x0_ext, "dd_cg_normal: x aliases an input");
-  const TileShape sh = dd_tiles(dd->Lext, dd->T);
-  const int tpc = sh.tiles_x * sh.tiles_t;
+  SCH_CHECK_ARG(ctx, dd->T % 8 == 0, "dd_cg_normal: T must be a multiple of 8");
+  TileShape sh;
+  dd_tile_shape(dd->Lext, dd->T, sh);
   const long long nsites = (long long)dd->S * dd->Lext * dd->T;
   const size_t vec = (size_t)nsites * 2 * sizeof(double2);
-  const int ntile_part = dd->S * tpc;
-  const size_t bytes = 3 * vec + sizeof(double) * (2 * (size_t)std::max(ntile_part, kRedGrid) +
-                                                   SC_COUNT + dd->S + 64) +
+  const size_t npart = (size_t)dd->S * dd->Lloc * dd->NC;   // row partials
+  const size_t bytes = 3 * vec + sizeof(double) * (2 * npart + SC_COUNT + dd->S + 64) +
                        sizeof(int) * (dd->S + 8) + 8 * 256;
   void* ws;
   int rc = sch_workspace(ctx, bytes, &ws);
@@ -821,8 +993,8 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   double2* r = (double2*)take(vec);
   double2* p = (double2*)take(vec);
   double2* ap = (double2*)take(vec);
-  double* part_a = (double*)take(sizeof(double) * std::max(ntile_part, kRedGrid));
-  double* part_b = (double*)take(sizeof(double) * std::max(ntile_part, kRedGrid));
+  double* part_a = (double*)take(sizeof(double) * npart);
+  double* part_b = (double*)take(sizeof(double) * npart);
   DDState st;
   st.sc = (double*)take(sizeof(double) * SC_COUNT);
   st.beta = (double*)take(sizeof(double) * dd->S);
@@ -830,28 +1002,27 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   st.ctl = (int*)take(sizeof(int) * 8);
   cudaStream_t s = ctx->stream;
   const int lo = kHalo, hi = kHalo + dd->Lloc;
-  const dim3 egrid(std::max(1, kRedGrid / dd->S), dd->S);   // elementwise passes: [S][gx] partials
-  const int gx = (int)egrid.x;
+  const unsigned egrid = chunk_grid((long long)dd->S * dd->Lext * dd->NC);   // warp-per-chunk passes
 
   // init: b (and x0) halos, then x, r, p on every row
   if ((rc = dd_exchange(ctx, dd, b_ext, 1, 4))) return rc;
   if (x0_ext && (rc = dd_exchange(ctx, dd, x0_ext, 1, 4))) return rc;
   k_dd_init<<<egrid, 256, 0, s>>>((const double2*)b_ext, (const double2*)x0_ext, (double2*)x_ext, r, p,
-                                  nsites, dd->T, dd->Lext, lo, hi, part_a);
+                                  dd->S, dd->Lext, dd->T, dd->CW, lo, hi, part_a);
   SCH_LAUNCHED(ctx);
-  if ((rc = dd_allsum(ctx, dd, part_a, gx, st.sc + SC_NORMB2))) return rc;
+  if ((rc = dd_allsum(ctx, dd, part_a, st.sc + SC_NORMB2))) return rc;
   TileArgs base = dd_tile_args(dd, sh, (const double2*)U_ext, m0);
   if (x0_ext) {   // r = b - A x0 on own rows, then p = r, both with fresh halos
     TileArgs tx = base;
     tx.in = (const double2*)x_ext;
     tx.bvec = (const double2*)b_ext;
     tx.out = r;
-    tx.partial = part_b;
-    launch_normal_tile<MODE_X>(sh, tx, s);
+    tx.rowpart = part_b;
+    launch_dd_tile<MODE_X>(sh, tx, s);
     SCH_LAUNCHED(ctx);
-    if ((rc = dd_allsum(ctx, dd, part_b, tpc, st.sc + SC_RR))) return rc;
+    if ((rc = dd_allsum(ctx, dd, part_b, st.sc + SC_RR))) return rc;
     if ((rc = dd_exchange(ctx, dd, (double*)r, 1, 4))) return rc;
-    k_dd_copy<<<egrid.x * egrid.y, 256, 0, s>>>(r, p, nsites);
+    k_dd_copy<<<egrid, 256, 0, s>>>(r, p, nsites);
     SCH_LAUNCHED(ctx);
   }
   k_dd_ctrl_init<<<1, 1, 0, s>>>(st, dd->S, tol, x0_ext != nullptr);
@@ -862,13 +1033,13 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   tp.in2 = p;
   tp.out = ap;
   tp.beta = st.beta;
-  tp.partial = part_a;
+  tp.rowpart = part_a;
   TileArgs txx = base;  // true residual / replacement pass
   txx.in = (const double2*)x_ext;
   txx.bvec = (const double2*)b_ext;
   txx.out = r;
   txx.flag = st.flag;
-  txx.partial = part_b;
+  txx.rowpart = part_b;
 
   // One iteration; the iteration number lives on the device (ctl[3]), so the
   // body is the same every time and can be captured.
@@ -888,19 +1059,19 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
     int e = SCH_OK;
     do {
       if ((e = dd_exchange(ctx, dd, (double*)r, 1, 4))) break;
-      launch_normal_tile<MODE_P>(sh, tp, q);
+      launch_dd_tile<MODE_P>(sh, tp, q);
       ctx->launches++;
-      if ((e = dd_allsum(ctx, dd, part_a, tpc, st.sc + SC_PAP, post(POST_ALPHA)))) break;
-      k_dd_update<<<egrid, 256, 0, q>>>(r, p, (double2*)x_ext, ap, st, nsites, dd->T, dd->Lext, lo,
-                                        hi, part_b);
+      if ((e = dd_allsum(ctx, dd, part_a, st.sc + SC_PAP, post(POST_ALPHA)))) break;
+      k_dd_update<<<egrid, 256, 0, q>>>(r, p, (double2*)x_ext, ap, st, dd->S, dd->Lext, dd->T, dd->CW,
+                                        lo, hi, part_b);
       ctx->launches++;
-      if ((e = dd_allsum(ctx, dd, part_b, gx, st.sc + SC_RR, post(POST_CHECK)))) break;
+      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, post(POST_CHECK)))) break;
       // x halos are current (x is updated on every row), so no exchange here
-      launch_normal_tile<MODE_X>(sh, txx, q);
+      launch_dd_tile<MODE_X>(sh, txx, q);
       ctx->launches++;
       // the final control also advances the iteration and, inside the WHILE
       // graph, sets the loop condition
-      if ((e = dd_allsum(ctx, dd, part_b, tpc, st.sc + SC_TN2, post(POST_FINAL, h)))) break;
+      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_TN2, post(POST_FINAL, h)))) break;
       cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) e = sch_fail(ctx, SCH_ERR_CUDA, "dd cg launch: %s", cudaGetErrorString(le));
     } while (0);

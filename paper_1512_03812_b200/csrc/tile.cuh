@@ -44,9 +44,38 @@ struct TileArgs {
   int tiles_t, tiles_per_chain;
   double diag;                      // 2 + m0
   int own_lo, own_hi;               // x rows written / summed; own_hi == 0 => all rows
+  // RP (decomposed lattice): instead of one partial per tile, one partial per
+  // (own row, TT-wide t-chunk), [B][own_hi-own_lo][T/TT], each the canonical
+  // tree sum (row_chunk_sum) of its TT site values — so the global sum
+  // (dd.cu) does not depend on how the lattice is cut into strips
+  double* __restrict__ rowpart;
 };
 
-template <int TX, int TT, int HX, int HT, int MODE, int NT>
+// Canonical deterministic sum of TT consecutive values p[0..TT) by one warp:
+// a balanced binary tree over the values in index order (zero padded to 32
+// lanes), i.e. adjacent pairs first.  Every kernel that forms a row-chunk
+// partial of the decomposed lattice uses this order, so the partial does
+// not depend on which kernel, tile or strip produced it.
+template <int TT>
+SCH_DEV double row_chunk_sum(const double* p, int lane) {
+  double v;
+  if constexpr (TT >= 64) {
+    constexpr int K = TT / 32;   // power of two
+    double a[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) a[k] = p[lane * K + k];
+#pragma unroll
+    for (int w = K / 2; w >= 1; w >>= 1)
+#pragma unroll
+      for (int k = 0; k < w; ++k) a[k] = a[2 * k] + a[2 * k + 1];
+    v = a[0];
+  } else {
+    v = lane < TT ? p[lane] : 0.0;
+  }
+  return warp_tree_sum(v);
+}
+
+template <int TX, int TT, int HX, int HT, int MODE, int NT, bool RP = false>
 __device__ __forceinline__ void tile_body(const TileArgs& a, int c, int tile, double2* E, int* gx,
                                           int* gxm, int* gt, int* gtm, double* slot) {
   constexpr int RX = TX + 2 * HX, RT = TT + 2 * HT, NR = RX * RT;
@@ -130,8 +159,10 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int c, int tile, do
 
   // ---- phase C: D^dag on the tile
   double part = 0.0;
+  double cv[CPT];   // RP: per-cell values, reduced per row after the loop
 #pragma unroll
   for (int j = 0; j < CPT; ++j) {
+    cv[j] = 0.0;
     const int k = threadIdx.x + j * NT;
     if (k >= NR) continue;
     const int ri = k / RT, rj = k - (k / RT) * RT;
@@ -147,22 +178,45 @@ __device__ __forceinline__ void tile_body(const TileArgs& a, int c, int tile, do
       Spinor bb = ld256_spinor_nc(a.bvec, site);
       r.s0 = csub(bb.s0, r.s0);
       r.s1 = csub(bb.s1, r.s1);
-      part += spinor_norm2(r);
+      cv[j] = spinor_norm2(r);
     } else if (MODE == MODE_P) {
-      part += spinor_redot(v[j], r);
+      cv[j] = spinor_redot(v[j], r);
     }
+    part += cv[j];
     st256_spinor(a.out, site, r);
   }
-  if (MODE != MODE_PLAIN) {
+  if (MODE != MODE_PLAIN && RP) {
+    __syncthreads();   // every read of the exports is done: reuse E for the cell values
+    double* val = reinterpret_cast<double*>(E);   // [TX][TT]
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      const int k = threadIdx.x + j * NT;
+      if (k >= NR) continue;
+      const int ri = k / RT, rj = k - (k / RT) * RT;
+      const int li = ri - HX, lj = rj - HT;
+      if (li < 0 || li >= TX || lj < 0 || lj >= TT) continue;
+      val[li * TT + lj] = cv[j];
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nown = a.own_hi - a.own_lo, nch = T / TT;
+    for (int li = warp; li < TX; li += NT / 32) {
+      const int x = x0 + li;
+      if (x >= L || x < a.own_lo || x >= a.own_hi) continue;   // warp-uniform
+      const double v = row_chunk_sum<TT>(val + li * TT, lane);
+      if (lane == 0) a.rowpart[((long long)c * nown + (x - a.own_lo)) * nch + tt] = v;
+    }
+  } else if (MODE != MODE_PLAIN) {
     double s = block_sum<NT>(part, slot);
     if (threadIdx.x == 0) a.partial[(long long)c * a.tiles_per_chain + tile] = s;
   }
 }
 
 // One CTA per tile.
-template <int TX, int TT, int HX, int HT, int MODE, int NT, int MINB>
+template <int TX, int TT, int HX, int HT, int MODE, int NT, int MINB, bool RP = false>
 __global__ void __launch_bounds__(NT, MINB) k_normal_tile(TileArgs a) {
   constexpr int RX = TX + 2 * HX, RT = TT + 2 * HT;
+  static_assert(!RP || 8 * RX * RT >= TX * TT, "row values must fit the export buffer");
   extern __shared__ double2 E[];            // [4][NR] exported projections (dynamic)
   __shared__ int gx[RX], gxm[RX], gt[RT], gtm[RT];
   __shared__ double slot[NT / 32];
@@ -170,7 +224,7 @@ __global__ void __launch_bounds__(NT, MINB) k_normal_tile(TileArgs a) {
   const int c = blockIdx.x / a.tiles_per_chain;
   const int tile = blockIdx.x - c * a.tiles_per_chain;
   if (MODE != MODE_PLAIN && a.flag && a.flag[c] == 0) return;
-  tile_body<TX, TT, HX, HT, MODE, NT>(a, c, tile, E, gx, gxm, gt, gtm, slot);
+  tile_body<TX, TT, HX, HT, MODE, NT, RP>(a, c, tile, E, gx, gxm, gt, gtm, slot);
 }
 
 // Persistent variant for sparse work (the CG true-residual pass, where only
@@ -265,6 +319,44 @@ inline void launch_tile_inst(const TileArgs& a, cudaStream_t st, int sparse_grid
   else
     launch_k(pdl, k_normal_tile<TX, TT, HX, HT, MODE, NT, MINB>, dim3((unsigned)a.B * a.tiles_per_chain),
              dim3(NT), smem, st, a);
+}
+
+// Decomposed lattice (dd.cu): tiles whose t-extent is the row-chunk width CW
+// of the canonical row partials (CW = 64, 32, 16 or 8 by T), x-clipped, with
+// RP row partials.  kind = CW.
+inline bool dd_tile_shape(int Lext, int T, TileShape& s) {
+  int tx, tt;
+  if (T % 64 == 0) { tx = 16; tt = 64; }
+  else if (T % 32 == 0) { tx = 16; tt = 32; }
+  else if (T % 16 == 0) { tx = 8; tt = 16; }
+  else if (T % 8 == 0) { tx = 8; tt = 8; }
+  else return false;
+  s = {tt, tx, tt, (Lext + tx - 1) / tx, T / tt};
+  return true;
+}
+
+template <int TX, int TT, int MODE, int NT, int MINB>
+inline void launch_dd_tile_inst(const TileArgs& a, cudaStream_t st) {
+  constexpr int NR = (TX + 4) * (TT + 4);
+  constexpr size_t smem = sizeof(double2) * 4 * NR;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_normal_tile<TX, TT, 2, 2, MODE, NT, MINB, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_normal_tile<TX, TT, 2, 2, MODE, NT, MINB, true>
+      <<<dim3((unsigned)a.B * a.tiles_per_chain), dim3(NT), smem, st>>>(a);
+}
+
+template <int MODE>
+inline void launch_dd_tile(const TileShape& sh, const TileArgs& a, cudaStream_t st) {
+  switch (sh.kind) {
+    case 64: launch_dd_tile_inst<16, 64, MODE, 512, 2>(a, st); break;
+    case 32: launch_dd_tile_inst<16, 32, MODE, 512, 2>(a, st); break;
+    case 16: launch_dd_tile_inst<8, 16, MODE, 128, 4>(a, st); break;
+    default: launch_dd_tile_inst<8, 8, MODE, 128, 4>(a, st); break;
+  }
 }
 
 // Launch the instantiation matching `sh`.  sparse_grid > 0 selects the

@@ -13,7 +13,8 @@ face exchanges it needs, so the same schedules drive both paths:
                   force-gradient contraction — each stencil's input faces
                   exchanged first
 * inner_leapfrog  micro steps with one q exchange after every drift
-* Hamiltonian     own-row sums per strip (sch_dd_own_sum) + a global sum
+* Hamiltonian     whole-lattice sums of the own rows (sch_dd_own_sum: the
+                  canonical tree, strip-count invariant)
 
 * kick_fg_full     gauge force, fermion force, C_GG (plaquettes two rows
                   out: the 2-row halo), the gauge Hessian dot f and both
@@ -34,7 +35,6 @@ from dataclasses import dataclass
 
 import numpy as np
 import torch
-import torch.distributed as dist
 
 from . import _lib
 from .dd import DDWilsonDirac, StripLattice
@@ -290,27 +290,18 @@ def _run_program(st: DDState, scheme: str, h: float, m: int, fgc: float):
             raise NotImplementedError(f"{name} in {scheme} is not wired for strips")
 
 
-def _global_sums(lat: StripLattice, per_strip: torch.Tensor) -> list[float]:
-    """Whole-lattice sums of the per-strip values (K, S): strips added in
-    strip order, then across the lattice's ranks (lat.group) — one
-    collective and one host read for all K sums."""
-    v = per_strip[:, 0].clone()
-    for s in range(1, lat.S):
-        v = v + per_strip[:, s]
-    if lat.world > 1:
-        dist.all_reduce(v, group=lat.group)
-    return v.tolist()
-
-
 def dd_hamiltonian(st: DDState) -> float:
-    """H = kin + S_G + S_F over the whole lattice (hmc.py:44-51)."""
+    """H = kin + S_G + S_F over the whole lattice (hmc.py:44-51).  Each sum is
+    formed on the device by the lattice's canonical tree through its
+    transport (sch_dd_own_sum), so every rank gets the same bits for any
+    number of strips; one host read for the three."""
     _, _, xi = st.solve_pair()
-    out = torch.empty((3, st.S), dtype=torch.float64, device=st.q.device)
-    _call("sch_dd_own_sum", st.lat._handle, 0, _lib.ptr(st.p), None, _lib.ptr(out[0]))
-    _call("sch_dd_own_sum", st.lat._handle, 1, _lib.ptr(st.q), None, _lib.ptr(out[1]))
-    _call("sch_dd_own_sum", st.lat._handle, 2, _lib.ptr(st.eta), _lib.ptr(xi), _lib.ptr(out[2]))
-    kin, gsum, s_f = _global_sums(st.lat, out)
-    return (kin + st.beta * gsum) + s_f
+    out = torch.empty((3,), dtype=torch.float64, device=st.q.device)
+    _call("sch_dd_own_sum", st.lat._handle, 0, _lib.ptr(st.p), None, _lib.ptr(out[0:1]))
+    _call("sch_dd_own_sum", st.lat._handle, 1, _lib.ptr(st.q), None, _lib.ptr(out[1:2]))
+    _call("sch_dd_own_sum", st.lat._handle, 2, _lib.ptr(st.eta), _lib.ptr(xi), _lib.ptr(out[2:3]))
+    psq, gsum, s_f = out.tolist()
+    return (0.5 * psq + st.beta * gsum) + s_f
 
 
 def dd_integrate(st: DDState, spec: IntegratorSpec, tau: float):

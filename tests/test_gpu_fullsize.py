@@ -16,8 +16,8 @@ do not need the oracle to redo the whole run:
 * cfg4 (1024 x 64^2, m0 = 0.02): per-chain CG (cluster engine): every
   chain's solution (<= 1e-12) and iteration count against the oracle.
 * cfg5 (2048^2): the decomposed D^dag D (local and peer-memory transports)
-  against the oracle on the whole lattice, and the decomposed CG's true
-  residual.
+  against the oracle on the whole lattice; the decomposed CG on 2 and 8
+  strips bit-identical to the one-strip solve, with its true residual.
 """
 
 import numpy as np
@@ -164,20 +164,44 @@ def test_cfg4_cluster_cg_every_chain_equals_oracle():
     assert err.max() < TOL_OP, (err.argmax(), err.max())
 
 
-@pytest.mark.parametrize("transport", ["local", "p2p"])
-def test_cfg5_decomposed_lattice_full_size(transport):
-    from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice
-    from oracle import schwinger_oracle as O
+@pytest.fixture(scope="module")
+def cfg5():
     L = 2048
     rng = np.random.default_rng(5)
     q = rng.uniform(-np.pi, np.pi, (2, L, L))
     psi = rng.standard_normal((L, L, 2)) + 1j * rng.standard_normal((L, L, 2))
-    lat = StripLattice(L, L, strips=2, transport=transport)
+    return L, q, psi
+
+
+@pytest.fixture(scope="module")
+def cfg5_one_strip(cfg5):
+    """The undecomposed (G = 1) solve of the 2048^2 lattice."""
+    from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice
+    L, q, psi = cfg5
+    lat = StripLattice(L, L, strips=1)
+    op = DDWilsonDirac(lat, lat.scatter_links(q), 0.05)
+    x, it, rel = op.cg(lat.scatter_spinor(psi), 1e-10)
+    return npy(lat.gather_spinor(x)), it, rel
+
+
+@pytest.mark.parametrize("transport,G", [("local", 2), ("p2p", 2), ("local", 8)])
+def test_cfg5_decomposed_lattice_full_size(cfg5, cfg5_one_strip, transport, G):
+    """2048^2 (configs[4]) on G strips: D^dag D against the oracle on the whole
+    lattice; the decomposed CG bit-identical to the one-strip solve (same
+    iteration count, same solution bits) and its true residual recomputed
+    by the oracle."""
+    from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice
+    from oracle import schwinger_oracle as O
+    L, q, psi = cfg5
+    lat = StripLattice(L, L, strips=G, transport=transport)
     op = DDWilsonDirac(lat, lat.scatter_links(q), 0.05)
     U = O.fermion_links(q)
     got = npy(lat.gather_spinor(op.normal(lat.scatter_spinor(psi))))
     assert rel_err(got, O.normal_op(U, psi, 0.05)) < TOL_OP
     x, it, rel = op.cg(lat.scatter_spinor(psi), 1e-10)
+    x = npy(lat.gather_spinor(x))
+    x1, it1, rel1 = cfg5_one_strip
+    assert it == it1 and rel == rel1 and np.array_equal(x, x1)
     assert rel <= 1e-10 and it > 0
-    rr = true_relres(O, U[None], 0.05, npy(lat.gather_spinor(x))[None], psi[None])
+    rr = true_relres(O, U[None], 0.05, x[None], psi[None])
     assert rr[0] <= 1.0001e-10, rr
