@@ -233,6 +233,58 @@ def cpu_baseline(seconds, outer):
                       "oracle/schwinger_oracle.py"}
 
 
+def _cpu_cg_iter_worker(args):
+    """Seconds per CG iteration of the CPU port on one L x L lattice (one
+    core): repeated capped cg_normal calls for ~seconds."""
+    L, m0, seconds, seed = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from oracle import schwinger_oracle as O
+    rng = O.make_rng(seed, 0)
+    U = O.fermion_links(O.hot_start(rng, L, L))
+    psi = rng.standard_normal((L, L, 2)) + 1j * rng.standard_normal((L, L, 2))
+    n, t0 = 0, time.perf_counter()
+    while True:
+        try:
+            O.cg_normal(U, m0, psi, 1e-30, maxiter=10)
+        except O.OracleSolverError:
+            pass
+        n += 10
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            return n, el
+
+
+def cpu_cg_rate(L, m0, seconds):
+    """SURVEY 8(d)(ii) for a workload whose CPU trajectory outlasts the
+    bench's budget (cfg4: a 64^2 light-fermion trajectory is minutes on one
+    core): every host core times the port's CG iteration; the trajectory
+    rate is extrapolated with the GPU run's CG iterations per trajectory
+    (finish_cpu_cg_rate).  The CG is >= 98 % of the CPU trajectory (SURVEY
+    8(a) a7), so this slightly favours the CPU."""
+    cores = cpu_cores()
+    with mp.get_context("fork").Pool(cores) as pool:
+        res = pool.map(_cpu_cg_iter_worker, [(L, m0, seconds, 99 + c) for c in range(cores)])
+    n = sum(r[0] for r in res)
+    per_core_rate = sum(r[0] / r[1] for r in res) / cores
+    return {"s_per_cg_iteration_per_core": 1.0 / per_core_rate, "cores": cores, "kind": "port",
+            "cg_iterations_timed": n, "L": L}
+
+
+def finish_cpu_cg_rate(rate, iters_per_chain_traj):
+    if rate is None:
+        return None
+    per_traj = rate["s_per_cg_iteration_per_core"] * iters_per_chain_traj
+    return {"value": rate["cores"] / per_traj, "unit": "chain-trajectories/s",
+            "cores": rate["cores"], "kind": "port",
+            "s_per_cg_iteration_per_core": rate["s_per_cg_iteration_per_core"],
+            "sample": f"{rate['cg_iterations_timed']} CG iterations of the port "
+                      f"(oracle/schwinger_oracle.py cg_normal) on hot-start {rate['L']}x"
+                      f"{rate['L']} lattices, {rate['cores']} processes; chain-trajectories/s "
+                      f"extrapolated = cores / (s per iteration x {iters_per_chain_traj:.0f} CG "
+                      "iterations per chain-trajectory of this GPU run) — an extrapolation, "
+                      "forces and kicks (< 2 % on CPU) not counted"}
+
+
 # BASELINE.json configs[0] ("cfg1"): the reference's own CPU run, one chain
 CFG1 = dict(L=16, T=16, beta=2.0, m0=0.1, tau=1.0, h=0.2, scheme="adapted-nested-fg",
             micro_per_call=2, cg_tol=1e-10)
@@ -677,7 +729,11 @@ def run_ours(args):
     hbm_peak, peak_kind = peaks()
 
     cpu = cpu_stencil = cpu1 = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    cpu_rate = None
+    if rank == 0 and world == 1 and not args.no_cpu and args.workload == "cfg4":
+        ph = WORKLOADS["cfg4"]["phys"]
+        cpu_rate = cpu_cg_rate(ph["L"], ph["m0"], args.cpu_seconds)   # before CUDA init
+    elif rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(args.cpu_seconds, args.outer)   # before CUDA init (fork-safe)
         if not args.no_stencil:
             cpu_stencil = cpu_stencil_baseline(min(args.cpu_seconds, 5.0))
@@ -921,6 +977,8 @@ def run_ours(args):
         if args.workload == "cfg3" and not sw.hmc.USE_MEGA:
             mega_leg = megakernel_leg(torch, sw, qs[0], drngs[0], cfg, value / world)
 
+    if cpu_rate is not None:
+        cpu = finish_cpu_cg_rate(cpu_rate, cg_iters / (chains * args.steps))
     if rank == 0:
         line = {
             "metric": "HMC trajectories/s", "value": value, "unit": "chain-trajectories/s",
@@ -1082,11 +1140,15 @@ def run_cfg5(args):
     w = WORKLOADS["cfg5"]["phys"]
     cfg = sw.HmcConfig(L=L, T=T, beta=w["beta"], m0=w["m0"], tau=w["tau"], h=w["tau"] / args.outer,
                        scheme=w["scheme"], micro_per_call=w["micro_per_call"], cg_tol=w["cg_tol"])
-    q_ext = lat.scatter_links(np.random.default_rng(5).uniform(-np.pi, np.pi, (2, L, T)))
+    # the reference's make_rng(5, 0) stream walked on the device: hot start,
+    # then the update's p / phi of the whole lattice (own rows kept) and the
+    # Metropolis uniform
+    drng = sw.NumpyDeviceRng(seed=5, n_chains=1, stream0=0)
+    q_ext = lat.scatter_links(drng.hot_start(sw.LatticeGeom(L, T))[0])
     sync()
     g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     g0.record()
-    q_ext, traj = dd_hmc_update(lat, q_ext, cfg, sw.make_rng(5, 0))
+    q_ext, traj = dd_hmc_update(lat, q_ext, cfg, drng)
     g1.record()
     sync()
     traj_ms = g0.elapsed_time(g1)
@@ -1115,8 +1177,9 @@ def run_cfg5(args):
                            "micro_per_call": cfg.micro_per_call, "tau": cfg.tau,
                            "ms": traj_ms, "trajectories_per_s": 1e3 / traj_ms, "dh": traj.dh,
                            "inversions": traj.inversions,
-                           "includes": "host heatbath draws of the full lattice (reference "
-                                       "generator), H at both ends, Metropolis"},
+                           "includes": "heatbath draws of the full lattice on the device "
+                                       "(the reference's Philox/ziggurat stream, csrc/nprng.cu), "
+                                       "H at both ends, Metropolis"},
             "cpu_baseline": None if cpu5 is None else {
                 "ddagd_GBs": 96.0 * sites / cpu5[0] / 1e9, "cg_s_per_iteration": cpu5[1],
                 "trajectory_s_extrapolated": cpu5[1] * iters * traj.inversions / 2,

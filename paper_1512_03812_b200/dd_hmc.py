@@ -41,7 +41,7 @@ from .dd import DDWilsonDirac, StripLattice
 from .fermion import InversionCounter, draw_phi
 from .hmc import TrajectoryStats, metropolis
 from .integrators import FG_KICK_SIGN, PROGRAMS, IntegratorSpec
-from .lattice import as_links, as_spinor
+from .lattice import LatticeGeom, NumpyDeviceRng, as_links, as_spinor
 
 SUPPORTED = ("leapfrog", "5stage", "5stage-fg", "fg-approx", "11stage", "nested-leapfrog",
              "nested-5stage", "nested-fg", "adapted-nested-fg")
@@ -317,10 +317,24 @@ def dd_integrate(st: DDState, spec: IntegratorSpec, tau: float):
 def dd_hmc_update(lat: StripLattice, q_ext, config, rng):
     """One HMC update of the decomposed lattice, drawing in the reference
     order from the full-lattice generator ``rng`` (hmc.py:69-95).  Returns
-    (links, TrajectoryStats); on reject the caller's links come back."""
+    (links, TrajectoryStats); on reject the caller's links come back.
+
+    ``rng`` is a host ``np.random.Generator`` or a one-stream
+    ``NumpyDeviceRng``: the device generator walks the same Philox/ziggurat
+    stream on the GPU (csrc/nprng.cu), so every rank draws the whole-lattice
+    p and phi there and keeps its own rows — the same values as the host
+    draws, no host generation or upload."""
     L, T = config.L, config.T
-    p_full = rng.standard_normal((2, L, T))
-    phi_full = None if config.quenched else draw_phi(rng, L, T)
+    device_rng = isinstance(rng, NumpyDeviceRng)
+    if device_rng:
+        if rng.n != 1:
+            raise ValueError(f"the decomposed lattice draws one stream, got {rng.n}")
+        p_dev, phi_dev = rng.heatbath(LatticeGeom(L, T), quenched=config.quenched)
+        p_full = p_dev[0]
+        phi_full = None if phi_dev is None else phi_dev[0]
+    else:
+        p_full = rng.standard_normal((2, L, T))
+        phi_full = None if config.quenched else draw_phi(rng, L, T)
     q_in = as_links(q_ext)
     q0 = lat.exchange(q_in.clone(), 2, 1)
     st = DDState(lat, q0, lat.scatter_links(p_full),
@@ -338,7 +352,14 @@ def dd_hmc_update(lat: StripLattice, q_ext, config, rng):
     wall = time.perf_counter() - t0
     h_end = dd_hamiltonian(st)
     dh = float(h_end - h_start)
-    accepted = metropolis(dh, rng)
+    if device_rng:   # hmc.py:54-60 on the device stream (one uniform iff dH > 0)
+        flag = int(rng.metropolis(torch.tensor([dh], dtype=torch.float64,
+                                               device=st.q.device)).item())
+        if flag < 0:
+            raise ValueError(f"non-finite energy change dH={dh}")
+        accepted = bool(flag)
+    else:
+        accepted = metropolis(dh, rng)
     stats = TrajectoryStats(dh=dh, accepted=accepted, inversions=inv, n_steps=n_steps,
                             wall_time=wall)
     return (st.q if accepted else q_ext), stats

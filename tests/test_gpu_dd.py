@@ -140,6 +140,33 @@ def test_dd_hmc_update_is_bit_identical_for_every_strip_count():
         assert np.array_equal(runs[G][1], runs[1][1]), G
 
 
+def test_dd_hmc_update_device_heatbath_equals_host_draws():
+    """The device NumPy-stream generator (one stream, whole lattice drawn on
+    the GPU, own rows kept) gives the same updates as the host generator:
+    same dH bits, accepts (the device Metropolis uniform included) and links,
+    over updates that both accept and reject."""
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200.dd import StripLattice
+    from paper_1512_03812_b200.dd_hmc import dd_hmc_update
+    from oracle import schwinger_oracle as O
+    L, G = 32, 4
+    cfg = sw.HmcConfig(L=L, T=L, beta=2.0, m0=0.1, tau=0.5, h=0.5, scheme="adapted-nested-fg",
+                       micro_per_call=2, cg_tol=1e-10)
+    lat = StripLattice(L, L, strips=G)
+    rng_h = O.make_rng(33, 0)
+    q0 = O.hot_start(rng_h, L, L)
+    rng_d = sw.NumpyDeviceRng(seed=33, n_chains=1, stream0=0)
+    assert np.array_equal(npy(rng_d.hot_start(sw.LatticeGeom(L, L))[0]), q0)
+    qh = qd = lat.scatter_links(q0)
+    for _ in range(4):
+        qh, sh = dd_hmc_update(lat, qh, cfg, rng_h)
+        qd, sd = dd_hmc_update(lat, qd, cfg, rng_d)
+        assert (sd.dh, sd.accepted, sd.inversions) == (sh.dh, sh.accepted, sh.inversions)
+        assert torch.equal(qd, qh)
+    with pytest.raises(ValueError):
+        dd_hmc_update(lat, qd, cfg, sw.NumpyDeviceRng(seed=1, n_chains=2))
+
+
 def test_dd_cg_zero_rhs_warm_start_and_cap():
     import paper_1512_03812_b200 as sw
     from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice

@@ -120,3 +120,27 @@ def test_gpu_sweep_matches_oracle_cells(experiment):
         m = O.measure_dh(q0, cfg, O.make_rng(cfg.seed, i * 1000 + j))
         assert abs(float(r[3]) - m["mean_abs"]) <= 1e-8 + 1e-6 * m["mean_abs"]
         assert int(r[6]) == m["inversions_per_traj"]
+
+
+def test_tune_acceptance_treats_cg_cap_as_rejection(experiment, monkeypatch):
+    """A cell whose CG hits the cap (a wild trajectory at large h) counts as
+    acceptance 0 in the bisection instead of aborting the tuning run."""
+    from paper_1512_03812_b200.fermion import SolverError
+    tmp, exp = experiment
+
+    def cell(q0, config, scheme, h, stream):
+        if h > 0.3:
+            raise SolverError("injected cap", 1e-9)
+        return SimpleNamespace(mean_abs=h**2, stderr=0.0, acceptance=1.0 - h, wall_per_traj=0.0,
+                               inversions_per_traj=8)
+
+    monkeypatch.setattr(H, "measure_cell", cell)
+    text = exp.read_text() + "h_min = 0.01\nh_max = 0.5\n"
+    exp.write_text(text)
+    out = tmp / "tune.csv"
+    res = CliRunner().invoke(H.main, ["tune-acceptance", "--config", str(exp), "--out", str(out)])
+    assert res.exit_code == 0, res.output
+    rows, _ = read_csv(out)
+    assert len(rows) == 1 + 2
+    for r in rows[1:]:
+        assert abs(float(r[8]) - 0.9) <= 0.02
