@@ -58,18 +58,18 @@ int launch_resident(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
-template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0, bool ROT = false, bool XS = false>
+template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0, bool ROT = false>
 int launch_resblk(sch_ctx* ctx, const ResArgs& a, int B) {
   constexpr int NT = LC * TC / (BX * BT);
-  const size_t smem = sizeof(double2) * (2 * (2 * BT + 2 * BX) + (XS ? 2 * BX * BT : 0)) * NT;
+  const size_t smem = sizeof(double2) * 2 * (2 * BT + 2 * BX) * NT;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB, TSH, ROT, XS>,
+    cudaError_t e = cudaFuncSetAttribute(k_cg_resblk<LC, TC, BX, BT, MINB, TSH, ROT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  k_cg_resblk<LC, TC, BX, BT, MINB, TSH, ROT, XS><<<B, NT, smem, ctx->stream>>>(a);
+  k_cg_resblk<LC, TC, BX, BT, MINB, TSH, ROT><<<B, NT, smem, ctx->stream>>>(a);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
@@ -117,15 +117,7 @@ int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
     tsh = (e && e[0] == '0') ? 0 : 1;
   }
   const bool rot = resblk_rot();
-  static int xs = -1;   // experiment: x in shared memory, N CTAs/SM (SCH_RESBLK_XS=N)
-  if (xs < 0) {
-    const char* e = getenv("SCH_RESBLK_XS");
-    xs = e ? atoi(e) : 0;
-  }
   if (!forced && a.L == 16 && a.T == 16) {
-    if (rot && xs == 4) return launch_resblk<16, 16, 2, 2, 4, 1, true, true>(ctx, a, B);
-    if (rot && xs == 5) return launch_resblk<16, 16, 2, 2, 5, 1, true, true>(ctx, a, B);
-    if (rot && xs == 6) return launch_resblk<16, 16, 2, 2, 6, 1, true, true>(ctx, a, B);
     if (rot) return launch_resblk<16, 16, 2, 2, 4, 1, true>(ctx, a, B);
     return tsh ? launch_resblk<16, 16, 2, 2, 4, 1>(ctx, a, B) : launch_resblk<16, 16, 2, 2, 4>(ctx, a, B);
   }
@@ -177,13 +169,13 @@ int launch_cluster(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
-template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = true, bool XS = false>
+template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = true>
 int launch_cluster_tx(sch_ctx* ctx, const ResArgs& a, int B) {
   constexpr int NT = LC * TC / (CS * BX * BT);
   constexpr int PL = (2 * BT + 2 * BX) * NT;
   constexpr int FACE = BT * (TC / BT);
-  const size_t smem = sizeof(double2) * (2 * PL + 8 * FACE + (XS ? 2 * BX * BT * NT : 0));
-  auto kern = k_cg_cluster_tx<LC, TC, CS, BX, BT, MINB, ROT, XS>;
+  const size_t smem = sizeof(double2) * (2 * PL + 8 * FACE);
+  auto kern = k_cg_cluster_tx<LC, TC, CS, BX, BT, MINB, ROT>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -216,8 +208,6 @@ int cluster_dispatch(sch_ctx* ctx, const ResArgs& a, int B) {
       return resblk_rot() ? launch_cluster_tx<64, 64, 4, 2, 2, 1>(ctx, a, B)
                           : launch_cluster_tx<64, 64, 4, 2, 2, 1, false>(ctx, a, B);
     if (cs == 8) return launch_cluster_tx<64, 64, 8, 2, 2, 2>(ctx, a, B);
-    // experiment: x in shared memory (SCH_CLUSTER=83: 8 CTAs, 3 per SM)
-    if (cs == 83) return launch_cluster_tx<64, 64, 8, 2, 2, 3, true, true>(ctx, a, B);
   }
   if (a.L == 64 && a.T == 64 && cs == 4) return launch_cluster<64, 64, 4, 2, 2, 1>(ctx, a, B);
   return -1;   // no cluster instantiation: use the streaming engine

@@ -333,7 +333,7 @@ SCH_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
-template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = false, bool XS = false>
+template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = false>
 __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX * BT), MINB)
     k_cg_cluster_tx(ResArgs a) {
   namespace cgx = cooperative_groups;
@@ -412,38 +412,14 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   };
 
   double2 u0[SPT], u1[SPT];
-  Spinor r[SPT], p[SPT];
-  // XS: x in shared memory after the receive buffers (as k_cg_resblk's XS):
-  // 8 registers per site fewer, so more CTAs (of other chains) share an SM
-  Spinor xr[XS ? 1 : SPT];
-  double2* xs = RXm + 4 * FACE;
-  auto xget = [&](int k) -> Spinor {
-    if constexpr (XS) {
-      Spinor v;
-      v.s0 = xs[(2 * k) * NT + tid];
-      v.s1 = xs[(2 * k + 1) * NT + tid];
-      return v;
-    } else {
-      return xr[k];
-    }
-  };
-  auto xset = [&](int k, const Spinor& v) {
-    if constexpr (XS) {
-      xs[(2 * k) * NT + tid] = v.s0;
-      xs[(2 * k + 1) * NT + tid] = v.s1;
-    } else {
-      xr[k] = v;
-    }
-  };
+  Spinor x[SPT], r[SPT], p[SPT];
   double bb = 0.0;
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
     u0[k] = cscale(ROT ? -1.0 : -0.5, __ldg(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
     u1[k] = cscale(-0.5, __ldg(a.U + 2 * cb + V + site(k)));
     r[k] = rot_in<ROT>(ldg_spinor(a.b, cb + site(k)));
-    Spinor z;
-    z.s0 = z.s1 = make_double2(0, 0);
-    xset(k, z);
+    x[k].s0 = x[k].s1 = make_double2(0, 0);
     bb += spinor_norm2(r[k]);
   }
   publish(bb, 2);
@@ -452,7 +428,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   const double target = a.tol * normb;
   if (normb == 0.0) {
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(xget(k)));
+    for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(x[k]));
     if (tid == 0 && rank == 0) {
       a.iters[c] = 0;
       a.relres[c] = 0.0;
@@ -529,12 +505,8 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   Spinor w[SPT];
   double rs = normb2;
   if (a.x0) {
-    Spinor x[SPT];
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      x[k] = rot_in<ROT>(ldg_spinor(a.x0, cb + site(k)));
-      xset(k, x[k]);
-    }
+    for (int k = 0; k < SPT; ++k) x[k] = rot_in<ROT>(ldg_spinor(a.x0, cb + site(k)));
     apply(x, w, nullptr);
     double rr = 0.0;
 #pragma unroll
@@ -586,7 +558,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
     if (!repl) {
       publish(rsn, 1);
 #pragma unroll
-      for (int k = 0; k < SPT; ++k) xset(k, sp_fma(alpha, p[k], xget(k)));
+      for (int k = 0; k < SPT; ++k) x[k] = sp_fma(alpha, p[k], x[k]);
       rs_new = total(1);
       check = rs_new <= t2lo;
       if (!check && rs_new <= t2hi) {
@@ -596,15 +568,10 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
       }
     } else {
 #pragma unroll
-      for (int k = 0; k < SPT; ++k) xset(k, sp_fma(alpha, p[k], xget(k)));
+      for (int k = 0; k < SPT; ++k) x[k] = sp_fma(alpha, p[k], x[k]);
     }
     if (check) {
-      {
-        Spinor x[SPT];
-#pragma unroll
-        for (int k = 0; k < SPT; ++k) x[k] = xget(k);
-        apply(x, w, nullptr);
-      }
+      apply(x, w, nullptr);
       double tn2 = 0.0;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
@@ -635,7 +602,7 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
     inv_rs = __drcp_rn(rs);
   }
 #pragma unroll
-  for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(xget(k)));
+  for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(x[k]));
   if (tid == 0 && rank == 0) {
     a.iters[c] = status == 0 ? it : a.maxiter;
     a.relres[c] = status == 0 ? relres : fmin(best, sqrt(rs) / normb);

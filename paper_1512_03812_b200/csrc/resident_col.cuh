@@ -91,7 +91,7 @@ SCH_DEV double part4_block_sum(double v, double* slot) {
   return part4_sum<NW>(slot);
 }
 
-template <int LC, int TC, int BX, int BT, int TSH, bool COH, bool ROT = false, bool XS = false>
+template <int LC, int TC, int BX, int BT, int TSH, bool COH, bool ROT = false>
 SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   using Blk = std::conditional_t<ROT, SiteBlockRot<BX, BT>, SiteBlock<BX, BT>>;
   // ROT: the solve runs in the sigma1-diagonal spin basis (block_stencil.cuh)
@@ -127,40 +127,14 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   const int ttm = bx * NBT + (bt + NBT - 1) % NBT;
 
   double2 u0[SPT], u1[SPT];
-  Spinor r[SPT], p[SPT];
-  // XS: the iterate x lives in shared memory after the two exchange stages
-  // ([k][component][thread], conflict-free), not in registers: it is read
-  // and written once per iteration (x += alpha p) and by the true-residual
-  // check, and its 8 registers per site let one more CTA fit per SM
-  Spinor xr[XS ? 1 : SPT];
-  double2* xs = sm + 2 * PL;
-  auto xget = [&](int k) -> Spinor {
-    if constexpr (XS) {
-      Spinor v;
-      v.s0 = xs[(2 * k) * NT + tid];
-      v.s1 = xs[(2 * k + 1) * NT + tid];
-      return v;
-    } else {
-      return xr[k];
-    }
-  };
-  auto xset = [&](int k, const Spinor& v) {
-    if constexpr (XS) {
-      xs[(2 * k) * NT + tid] = v.s0;
-      xs[(2 * k + 1) * NT + tid] = v.s1;
-    } else {
-      xr[k] = v;
-    }
-  };
+  Spinor x[SPT], r[SPT], p[SPT];
   double bb = 0.0;
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
     u0[k] = cscale(ROT ? -1.0 : -0.5, res_ld2<COH>(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
     u1[k] = cscale(-0.5, res_ld2<COH>(a.U + 2 * cb + V + site(k)));
     r[k] = ld_b(cb + site(k));
-    Spinor z;
-    z.s0 = z.s1 = make_double2(0, 0);
-    xset(k, z);
+    x[k].s0 = x[k].s1 = make_double2(0, 0);
     bb += spinor_norm2(r[k]);
   }
   const double normb2 = block_sum<NT>(bb, red[0]);
@@ -168,7 +142,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   const double target = a.tol * normb;
   if (normb == 0.0) {   // fermion.py:181-182, per chain
 #pragma unroll
-    for (int k = 0; k < SPT; ++k) st_x(cb + site(k), xget(k));
+    for (int k = 0; k < SPT; ++k) st_x(cb + site(k), x[k]);
     if (tid == 0) {
       a.iters[c] = 0;
       a.relres[c] = 0.0;
@@ -238,12 +212,10 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   Spinor w[SPT];
   double rs = normb2;   // r = b exactly: the same sum as ||b||^2 (fermion.py:186,191)
   if (a.x0) {
-    Spinor x[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       x[k] = res_ld_spinor<COH>(a.x0, cb + site(k));
       if constexpr (ROT) x[k] = spin_rot(x[k]);
-      xset(k, x[k]);
     }
     normal_op(x, w);
     double rr = 0.0;
@@ -293,7 +265,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
     double nrm[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-      xset(k, sp_fma(alpha, p[k], xget(k)));
+      x[k] = sp_fma(alpha, p[k], x[k]);
       if (!repl) {
         r[k] = sp_fma(-alpha, w[k], r[k]);
         nrm[k] = spinor_norm2(r[k]);
@@ -319,12 +291,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
       }
     }
     if (check) {   // true residual b - A x (shared with the residual replacement)
-      {
-        Spinor x[SPT];
-#pragma unroll
-        for (int k = 0; k < SPT; ++k) x[k] = xget(k);
-        normal_op(x, w);
-      }
+      normal_op(x, w);
       double tn2 = 0.0;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
@@ -336,7 +303,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
       if (!repl || tn <= target) best = tn / normb;
       if (tn <= target) {
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) st_x(cb + site(k), xget(k));
+        for (int k = 0; k < SPT; ++k) st_x(cb + site(k), x[k]);
         if (tid == 0) {
           a.iters[c] = it;
           a.relres[c] = tn / normb;
@@ -359,7 +326,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
     inv_rs = __drcp_rn(rs);
   }
 #pragma unroll
-  for (int k = 0; k < SPT; ++k) st_x(cb + site(k), xget(k));
+  for (int k = 0; k < SPT; ++k) st_x(cb + site(k), x[k]);
   if (tid == 0) {
     a.iters[c] = a.maxiter;
     a.relres[c] = fmin(best, sqrt(rs) / normb);
@@ -367,8 +334,8 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
   }
 }
 
-template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0, bool ROT = false, bool XS = false>
+template <int LC, int TC, int BX, int BT, int MINB, int TSH = 0, bool ROT = false>
 __global__ void __launch_bounds__(LC * TC / (BX * BT), MINB) k_cg_resblk(ResArgs a) {
   extern __shared__ double2 sm[];
-  cg_resblk_run<LC, TC, BX, BT, TSH, false, ROT, XS>(a, blockIdx.x, (long long)blockIdx.x * LC * TC, sm);
+  cg_resblk_run<LC, TC, BX, BT, TSH, false, ROT>(a, blockIdx.x, (long long)blockIdx.x * LC * TC, sm);
 }

@@ -176,7 +176,9 @@ class DDWilsonDirac:
     def normal(self, psi_ext) -> torch.Tensor:
         """D^dag D on the own rows (halo rows of the output are not written)."""
         psi = as_spinor(psi_ext)
-        out = torch.zeros_like(psi)
+        out = torch.empty_like(psi)   # own rows written by the kernel, halo rows zeroed here
+        out[:, :HALO].zero_()
+        out[:, HALO + self.lat.Lloc:].zero_()
         _lib.ctx().call("sch_dd_ddagd", self.lat._handle, _lib.ptr(self.U), _lib.ptr(psi),
                         _lib.ptr(out), self.m0)
         return out
