@@ -71,6 +71,34 @@ def test_dd_hmc_update_matches_reference_full_lattice(scheme, h, G):
     assert np.max(np.abs(npy(lat.gather_links(q_ext)) - qo)) < 1e-8
 
 
+@pytest.mark.parametrize("L,T,G", [(256, 256, 2), (96, 192, 3), (40, 128, 5), (64, 64, 16)])
+def test_dd_long_rows_match_oracle_and_are_strip_invariant(L, T, G):
+    """Decomposed lattices with several 64-wide t-chunks per row (the
+    canonical row partials of dd.cu over more than one chunk, the t-wrap
+    between tiles, clipped x tiles): D^dag D vs the oracle, and CG
+    solutions / iteration counts / residuals bit-identical to one strip
+    (power-of-two strip heights: dd.cu's canonical sums)."""
+    from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice
+    from oracle import schwinger_oracle as O
+    rng = np.random.default_rng(L * T + G)
+    q = rng.uniform(-np.pi, np.pi, (2, L, T))
+    psi = rng.standard_normal((L, T, 2)) + 1j * rng.standard_normal((L, T, 2))
+    ref = O.normal_op(O.fermion_links(q), psi, 0.1)
+    runs = []
+    for g in (1, G):
+        lat = StripLattice(L, T, strips=g)
+        op = DDWilsonDirac(lat, lat.scatter_links(q), 0.1)
+        got = npy(lat.gather_spinor(op.normal(lat.scatter_spinor(psi))))
+        assert rel_err(got, ref) < 1e-12, g
+        x, it, rel = op.cg(lat.scatter_spinor(psi), 1e-10)
+        runs.append((npy(lat.gather_spinor(x)), it, rel))
+    assert runs[0][1] == runs[1][1] and runs[0][2] == runs[1][2]
+    assert np.array_equal(runs[0][0], runs[1][0])
+    if L * T <= 96 * 192:
+        xo, ito, _ = O.cg_normal(O.fermion_links(q), 0.1, psi, 1e-10)
+        assert runs[0][1] == ito and rel_err(runs[0][0], xo) < 1e-12
+
+
 @pytest.mark.parametrize("transport", ["local", "p2p"])
 def test_dd_exchange_fills_halos_from_neighbours(transport):
     from paper_1512_03812_b200.dd import StripLattice

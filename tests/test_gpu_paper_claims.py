@@ -203,7 +203,13 @@ def test_paper_scale_qualitative():
     sizes inside the published bands, and the nested force-gradient pair the
     cheapest in inversions per trajectory at 90 % acceptance."""
     import paper_1512_03812_b200 as sw
-    cfg = sw.HmcConfig(n_thermalize=500, h=0.05)
+    # SCHWINGER_PAPER_TOL: the CG tolerance (the paper's 1e-12 by default).
+    # At 1e-12 the batched solves of the force-gradient schemes' Z pair hit
+    # the float64 floor on 32x32 at this mass — the reference raises
+    # SolverError there too (profiles/r02/paper_scale/README.md) — so the
+    # recorded run uses 1e-10.
+    tol = float(os.environ.get("SCHWINGER_PAPER_TOL", "1e-12"))
+    cfg = sw.HmcConfig(n_thermalize=500, h=0.05, cg_tol=tol)
     q0, _ = sw.thermalize(cfg, sw.make_rng(cfg.seed, 0), on_solver_error="reject")
     pairs = [("leapfrog", "nested-leapfrog"), ("5stage", "nested-5stage"),
              ("5stage-fg", "nested-fg")]
