@@ -52,6 +52,7 @@
 #include "common.cuh"
 #include "runtime.hpp"
 #include "tile.cuh"
+#include "tma2d.cuh"
 #include "tma_tile.cuh"
 #include "../../include/schwinger_sm100.h"
 
@@ -600,14 +601,14 @@ __global__ void k_dd_tree_post(const double* __restrict__ vals, int G, double* _
 // the global sum of the row partials `part` ([S][Lloc][NC]) into *out (on
 // the device, every rank); `post` runs on the sum
 int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, double* out,
-              const DDPost& post = DDPost{}) {
+              const DDPost& post = DDPost{}, int nch = 0) {
   if (!dd->p2p && dd->comm == nullptr && dd->nranks > 1)
     return sch_fail(ctx, SCH_ERR_ARG, "dd: no transport (NCCL id or p2p connect)");
   RowRed a;
   a.part = part;
   a.S = dd->S;
   a.Lloc = dd->Lloc;
-  a.nch = dd->NC;
+  a.nch = nch > 0 ? nch : dd->NC;   // chunks per row of `part` (any power-of-two width: same tree)
   a.nb = (dd->Lloc + kRowBlk - 1) / kRowBlk;
   a.blk = dd->red_blk;
   a.ctr = dd->red_ctr;
@@ -776,6 +777,11 @@ __global__ void k_dd_own_sum(int kind, const double* __restrict__ a, const doubl
 inline unsigned chunk_grid(long long items) {
   return (unsigned)std::max<long long>(1, std::min<long long>((items + 7) / 8, 148 * 8));
 }
+
+// The TMA-pipelined 2-D tile pass (tma2d.cuh) for the D^dag D and the CG's
+// stencil pass (T a multiple of 32); SCH_DD_TMA2D=0 keeps the
+// one-tile-per-CTA halo kernel
+bool dd_use_tma2d(const sch_dd* dd) { return tma2d_enabled() && tma2d_shape_ok(dd->Lloc, dd->T); }
 
 TileArgs dd_tile_args(sch_dd* dd, const TileShape& sh, const double2* U, double m0) {
   TileArgs a{};
@@ -964,7 +970,8 @@ int sch_dd_ddagd(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* psi_ext,
   TileArgs a = dd_tile_args(dd, sh, (const double2*)U_ext, m0);
   a.in = (const double2*)psi_ext;
   a.out = (double2*)out_ext;
-  launch_dd_tile<MODE_PLAIN>(sh, a, ctx->stream);
+  if (!(dd_use_tma2d(dd) && launch_dd_tma2d<MODE_PLAIN>(a, ctx->stream, ctx->num_sms)))
+    launch_dd_tile<MODE_PLAIN>(sh, a, ctx->stream);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
@@ -979,7 +986,9 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   dd_tile_shape(dd->Lext, dd->T, sh);
   const long long nsites = (long long)dd->S * dd->Lext * dd->T;
   const size_t vec = (size_t)nsites * 2 * sizeof(double2);
-  const size_t npart = (size_t)dd->S * dd->Lloc * dd->NC;   // row partials
+  const bool t2d = dd_use_tma2d(dd);
+  const int nch_p = t2d ? dd->T / kT2T : dd->NC;            // chunks per row of the stencil pass
+  const size_t npart = (size_t)dd->S * dd->Lloc * std::max(dd->NC, nch_p);   // row partials
   const size_t bytes = 3 * vec + sizeof(double) * (2 * npart + SC_COUNT + dd->S + 64) +
                        sizeof(int) * (dd->S + 8) + 8 * 256;
   void* ws;
@@ -1060,9 +1069,9 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
     int e = SCH_OK;
     do {
       if ((e = dd_exchange(ctx, dd, (double*)r, 1, 4))) break;
-      launch_dd_tile<MODE_P>(sh, tp, q);
+      if (!(t2d && launch_dd_tma2d<MODE_P>(tp, q, ctx->num_sms))) launch_dd_tile<MODE_P>(sh, tp, q);
       ctx->launches++;
-      if ((e = dd_allsum(ctx, dd, part_a, st.sc + SC_PAP, post(POST_ALPHA)))) break;
+      if ((e = dd_allsum(ctx, dd, part_a, st.sc + SC_PAP, post(POST_ALPHA), t2d ? nch_p : 0))) break;
       k_dd_update<<<egrid, 256, 0, q>>>(r, p, (double2*)x_ext, ap, st, dd->S, dd->Lext, dd->T, dd->CW,
                                         lo, hi, part_b);
       ctx->launches++;

@@ -100,7 +100,8 @@ class StripLattice:
             if self.rank == 0:
                 ctx.call("sch_nccl_unique_id", ctypes.cast(buf, ctypes.c_void_p))
             obj = [bytes(buf.raw)]
-            dist.broadcast_object_list(obj, src=0, group=group)
+            src = 0 if group is None else dist.get_global_rank(group, 0)   # the group's rank 0
+            dist.broadcast_object_list(obj, src=src, group=group)
             nid = ctypes.create_string_buffer(obj[0], 128)
         handle = ctypes.c_void_p()
         ctx.call("sch_dd_create", None if nid is None else ctypes.cast(nid, ctypes.c_void_p),

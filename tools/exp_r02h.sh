@@ -1,0 +1,16 @@
+#!/bin/bash
+set -u
+O=gpurun_out/exp_r02h
+mkdir -p $O
+timeout 1200 python -m pytest tests/test_gpu_dd.py tests/test_gpu_fullsize.py -q -m gpu -x -p no:cacheprovider -k "dd or cfg5" > $O/pytest_dd.txt 2>&1
+tail -2 $O/pytest_dd.txt
+python bench.py --workload cfg5 --steps 5 --warmup 2 > $O/cfg5.log 2>&1
+grep '^{' $O/cfg5.log > $O/bench_cfg5_r02.json
+SCH_DD_TMA2D=0 python bench.py --workload cfg5 --steps 5 --warmup 2 --no-cpu > $O/cfg5_tile.log 2>&1
+for f in $O/cfg5.log $O/cfg5_tile.log; do grep '^{' $f | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['roofline']['frac'], d['cg'], d['trajectory']['ms'])"; done
+SCH_NO_CG_GRAPH=1 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/dd_launches.csv \
+  python tools/prof_dd.py local 1 > /dev/null 2>&1
+python tools/ncu_summary.py launches $O/dd_launches.csv | head -10
+SCH_NO_CG_GRAPH=1 ncu --set full --clock-control none --import-source on -k regex:k_dd_tma2d -s 4 -c 1 \
+  -o $O/ncu_dd_tma2d_p python tools/prof_dd.py local 1 > /dev/null 2>&1
+python tools/ncu_summary.py report $O/ncu_dd_tma2d_p.ncu-rep | head -24
