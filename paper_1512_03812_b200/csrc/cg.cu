@@ -111,19 +111,14 @@ int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
   const ResidentForce& rf = resident_force();
   const int fnt = rf.nt, fspt = rf.spt, fminb = rf.minb, fspec = rf.spec;
   const bool forced = resident_forced(V);
-  static int tsh = -1;   // t-faces through warp shuffles (default; SCH_RESBLK_TSH=0: SMEM)
-  if (tsh < 0) {
-    const char* e = getenv("SCH_RESBLK_TSH");
-    tsh = (e && e[0] == '0') ? 0 : 1;
-  }
   const bool rot = resblk_rot();
   if (!forced && a.L == 16 && a.T == 16) {
     if (rot) return launch_resblk<16, 16, 2, 2, 4, 1, true>(ctx, a, B);
-    return tsh ? launch_resblk<16, 16, 2, 2, 4, 1>(ctx, a, B) : launch_resblk<16, 16, 2, 2, 4>(ctx, a, B);
+    return launch_resblk<16, 16, 2, 2, 4, 1>(ctx, a, B);
   }
   if (!forced && a.L == 32 && a.T == 32) {
     if (rot) return launch_resblk<32, 32, 2, 2, 1, 1, true>(ctx, a, B);
-    return tsh ? launch_resblk<32, 32, 2, 2, 1, 1>(ctx, a, B) : launch_resblk<32, 32, 2, 2, 1>(ctx, a, B);
+    return launch_resblk<32, 32, 2, 2, 1, 1>(ctx, a, B);
   }
   int nt, spt, minb;
   bool spec = true;
@@ -152,24 +147,6 @@ int resident_dispatch(sch_ctx* ctx, const ResArgs& a, int B, long long V) {
 
 // Cluster-resident CG (resident_cluster.cuh): CS CTAs per chain.
 template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = true>
-int launch_cluster(sch_ctx* ctx, const ResArgs& a, int B) {
-  constexpr int NT = LC * TC / (CS * BX * BT);
-  const size_t smem = sizeof(double2) * 2 * (2 * BT + 2 * BX) * NT;
-  auto kern = k_cg_cluster<LC, TC, CS, BX, BT, MINB, ROT>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    if (e == cudaSuccess && CS > 8)
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e != cudaSuccess) return sch_fail(ctx, SCH_ERR_CUDA, "cluster attr: %s", cudaGetErrorString(e));
-    attr = true;
-  }
-  kern<<<B * CS, NT, smem, ctx->stream>>>(a);
-  SCH_LAUNCHED(ctx);
-  return SCH_OK;
-}
-
-template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = true>
 int launch_cluster_tx(sch_ctx* ctx, const ResArgs& a, int B) {
   constexpr int NT = LC * TC / (CS * BX * BT);
   constexpr int PL = (2 * BT + 2 * BX) * NT;
@@ -189,27 +166,12 @@ int launch_cluster_tx(sch_ctx* ctx, const ResArgs& a, int B) {
   return SCH_OK;
 }
 
-// 64^2 (cfg4): which cluster shape; SCH_CLUSTER=0 falls back to streaming,
-// SCH_CLUSTER_SYNC=1 selects the cluster-barrier variant
+// 64^2 (cfg4): the 4-CTA cluster kernel (measured: 62.2 ns per chain-
+// iteration; 8-CTA clusters 62.6, the cluster-barrier variant 78.5)
 int cluster_dispatch(sch_ctx* ctx, const ResArgs& a, int B) {
-  static int cs = -1;
-  if (cs < 0) {
-    cs = 4;   // measured (cfg4 shape): st.async/mbarrier variant 4 CTAs 67.2 ns/chain-iteration,
-              // 8 CTAs 67.8; cluster-barrier variant (4 CTAs) 78.5
-    if (const char* e = getenv("SCH_CLUSTER")) cs = atoi(e);
-  }
-  static int sync_mode = -1;
-  if (sync_mode < 0) {
-    const char* e = getenv("SCH_CLUSTER_SYNC");
-    sync_mode = (e && e[0] == '1') ? 1 : 0;
-  }
-  if (a.L == 64 && a.T == 64 && !sync_mode) {
-    if (cs == 4)
-      return resblk_rot() ? launch_cluster_tx<64, 64, 4, 2, 2, 1>(ctx, a, B)
-                          : launch_cluster_tx<64, 64, 4, 2, 2, 1, false>(ctx, a, B);
-    if (cs == 8) return launch_cluster_tx<64, 64, 8, 2, 2, 2>(ctx, a, B);
-  }
-  if (a.L == 64 && a.T == 64 && cs == 4) return launch_cluster<64, 64, 4, 2, 2, 1>(ctx, a, B);
+  if (a.L == 64 && a.T == 64)
+    return resblk_rot() ? launch_cluster_tx<64, 64, 4, 2, 2, 1>(ctx, a, B)
+                        : launch_cluster_tx<64, 64, 4, 2, 2, 1, false>(ctx, a, B);
   return -1;   // no cluster instantiation: use the streaming engine
 }
 
@@ -579,7 +541,7 @@ __global__ void k_zero_x_if_null(ElemArgs e, StreamState st) {
 int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, const double2* x0,
                  int B, int L, int T, double m0, double tol, int maxiter, int global_mode, int* iters,
                  double* relres, int* status) {
-  const TileShape sh = pick_tile(L, T, use_tma_cg());
+  const TileShape sh = pick_tile(L, T);
   const int tpc = sh.tiles_x * sh.tiles_t;
   const long long V = (long long)L * T;
   const size_t nvec = (size_t)B * V * 2;   // double2 per vector
@@ -656,10 +618,6 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
   const bool pt = tpc <= kSmallTpc;
   const unsigned cgrid = pt ? blocks_for(B, 128) : (unsigned)B;
   const int sparse = ctx->num_sms * 2;   // persistent grid of the true-residual pass
-  // TMA-pipelined stencil pass when its tiling equals the elementwise tiling
-  int tma_tx = 0;
-  const bool tma_p = use_tma_cg() && tma_tile_shape(L, T, tma_tx) && tma_tx == sh.TX &&
-                     sh.tiles_t == 1;
   if (pt) k_ctrl_init<true><<<cgrid, 128, 0, s>>>(st, x0 != nullptr);
   else k_ctrl_init<false><<<cgrid, 128, 0, s>>>(st, x0 != nullptr);
   SCH_LAUNCHED(ctx);
@@ -689,8 +647,7 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
   const bool pdl = use_pdl();
   auto enqueue_iteration = [&](cudaStream_t q) -> int {
     int n = 0;
-    if (tma_p) launch_normal_tma<MODE_P>(tp, q, ctx->num_sms);
-    else launch_normal_tile<MODE_P>(sh, tp, q, 0, pdl);
+    launch_normal_tile<MODE_P>(sh, tp, q, 0, pdl);
     ++n;
     if (pt) {
       launch_k(pdl, k_cg_update<true>, dim3(ngrid), dim3(256), 0, q, e, st);
@@ -728,14 +685,9 @@ int cg_streaming(sch_ctx* ctx, const double2* U, const double2* b, double2* x, c
     // The whole loop on the device: a conditional WHILE node whose body is
     // kBody captured iterations plus k_set_continue.  One graph launch per
     // solve, no host polling: the call returns without synchronising.
-    static int kb = -1;
-    if (kb < 0) {
-      const char* ev = getenv("SCH_CG_BODY");
-      kb = ev ? atoi(ev) : 0;
-    }
     // 4 iterations per pass of the WHILE body: the conditional node costs
     // ~3.5 us per evaluation, a converged iteration is a few no-op launches
-    const int kBody = kb > 0 ? kb : 4;
+    constexpr int kBody = 4;
     if (!ctx->cap_stream)
       SCH_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
     cudaGraph_t graph;

@@ -6,23 +6,18 @@
 // thread a BX x BT block of sites, with the block-owned exchange of
 // resident_col.cuh: faces are exported to shared memory, hops between a
 // thread's own sites stay in registers.  The x-faces of a CTA's first and
-// last row are read by the neighbouring CTA directly from its shared memory
-// (DSMEM, cluster.map_shared_rank), so the exchange never touches L2/HBM.
-//
-// Every __syncthreads of the single-CTA kernel becomes a cluster barrier
-// (barrier.cluster.arrive.release / wait.acquire); the global sums are
-// published the same way: each warp writes its partial into slot
-// [rank][warp] of every CTA of the cluster, and after the barrier each warp
-// sums the CS*NW slots in lane order (identical in every thread of the
-// cluster, so all CTAs take the same branch at every stopping test).
-//
-// Stopping rule, residual replacement and true-residual check are those of
-// the reference cg_normal (fermion.py:171-217), as in resident.cuh.
+// last row go to the neighbouring CTAs' shared memory (DSMEM), so the
+// exchange never touches L2/HBM; the global sums are published into every
+// CTA of the cluster and summed there in lane order (identical in every
+// thread of the cluster, so all CTAs take the same branch at every stopping
+// test).  Stopping rule, residual replacement and true-residual check are
+// those of the reference cg_normal (fermion.py:171-217), as in resident.cuh.
 //
 // ROT = true (the dispatch default, cg.cu resblk_rot) runs the solve in the
 // sigma1-diagonal spin basis of block_stencil.cuh (SiteBlockRot): b' = T b
 // in, x = T x' / 2 out, u0 prescaled by -1; 64^2 67.1 -> 62.2 ns per
-// chain-iteration.
+// chain-iteration.  (A variant synchronising with cluster-wide barriers
+// measured 78.5 ns, 8-CTA clusters 67.8: removed.)
 #pragma once
 
 #include <cooperative_groups.h>
@@ -36,268 +31,9 @@ SCH_DEV void cluster_barrier() {
   cluster_arrive();
   cluster_wait();
 }
-// 32-bit shared::cluster addressing (keeps the four neighbour bases in 4
-// registers instead of 4 generic 64-bit pointers)
-SCH_DEV uint32_t mapa_u32(const void* local, int rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-               : "=r"(r)
-               : "r"((uint32_t)__cvta_generic_to_shared(local)), "r"(rank));
-  return r;
-}
-SCH_DEV double2 ld_dsmem(uint32_t addr) {
-  double2 v;
-  asm volatile("ld.shared::cluster.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
-  return v;
-}
-
-template <int LC, int TC, int CS, int BX, int BT, int MINB, bool ROT = false>
-__global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX * BT), MINB)
-    k_cg_cluster(ResArgs a) {
-  namespace cgx = cooperative_groups;
-  constexpr int R = LC / CS;                  // x-rows per CTA
-  constexpr int SPT = BX * BT;
-  constexpr int NT = R * TC / SPT;
-  constexpr int NBT = TC / BT, NBX = R / BX;
-  constexpr int V = LC * TC;
-  constexpr int NW = NT / 32;
-  constexpr int NP = CS * NW;                 // partial-sum slots per reduction
-  constexpr int PL = (2 * BT + 2 * BX) * NT;  // double2 per exchange stage
-  static_assert(LC % CS == 0 && R % BX == 0 && TC % BT == 0 && NT % 32 == 0, "block shape");
-  static_assert(NP <= 32, "one partial per lane");
-  constexpr int O0 = 0, O1 = BT * NT, O2 = 2 * BT * NT, O3 = (2 * BT + BX) * NT;
-  extern __shared__ double2 sm[];
-  __shared__ double red[3][NP];
-  double2* E0 = sm;
-  double2* E1 = sm + PL;
-  cgx::cluster_group cluster = cgx::this_cluster();
-  const int rank = (int)cluster.block_rank();
-  const int tid = threadIdx.x;
-  const int c = blockIdx.x / CS;
-  const long long cb = (long long)c * V;
-  const int bx = tid / NBT, bt = tid % NBT;
-  auto site = [&](int k) {
-    return (rank * R + bx * BX + k / BT) * TC + bt * BT + k % BT;
-  };
-  // x-neighbour blocks: the next/previous block row of this CTA, or the
-  // first/last block row of the neighbouring CTA (periodic over the cluster)
-  const bool xp_remote = bx == NBX - 1, xm_remote = bx == 0;
-  const int txp = xp_remote ? bt : tid + NBT;
-  const int txm = xm_remote ? (NBX - 1) * NBT + bt : tid - NBT;
-  const int ttp = bx * NBT + (bt + 1) % NBT;
-  const int ttm = bx * NBT + (bt + NBT - 1) % NBT;
-  // shared::cluster bases of the x-face planes this thread reads (its own
-  // CTA's for interior block rows); stage 1 is E0, stage 2 E1 = E0 + PL
-  const int rp = xp_remote ? (rank + 1) % CS : rank;
-  const int rm = xm_remote ? (rank + CS - 1) % CS : rank;
-  const uint32_t Xp = mapa_u32(E0 + O0 + txp, rp);
-  const uint32_t Xm = mapa_u32(E0 + O1 + txm, rm);
-
-  // publish this warp's partial of v into slot [rank][warp] of every CTA;
-  // total() after the next cluster barrier
-  auto publish = [&](double v, int j) {
-    v = warp_sum(v);
-    if ((tid & 31) == 0) {
-      const int idx = rank * NW + (tid >> 5);
-#pragma unroll
-      for (int r = 0; r < CS; ++r) cluster.map_shared_rank(&red[j][0], r)[idx] = v;
-    }
-  };
-  auto total = [&](int j) {
-    const int l = tid & 31;
-    return warp_sum(l < NP ? red[j][l] : 0.0);
-  };
-
-  double2 u0[SPT], u1[SPT];
-  Spinor x[SPT], r[SPT], p[SPT];
-  double bb = 0.0;
-#pragma unroll
-  for (int k = 0; k < SPT; ++k) {
-    u0[k] = cscale(ROT ? -1.0 : -0.5, __ldg(a.U + 2 * cb + site(k)));   // exact: power-of-two scale
-    u1[k] = cscale(-0.5, __ldg(a.U + 2 * cb + V + site(k)));
-    r[k] = rot_in<ROT>(ldg_spinor(a.b, cb + site(k)));
-    x[k].s0 = x[k].s1 = make_double2(0, 0);
-    bb += spinor_norm2(r[k]);
-  }
-  publish(bb, 2);
-  cluster_barrier();
-  const double normb2 = total(2);
-  const double normb = sqrt(normb2);
-  const double target = a.tol * normb;
-  if (normb == 0.0) {   // fermion.py:181-182, per chain
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(x[k]));
-    if (tid == 0 && rank == 0) {
-      a.iters[c] = 0;
-      a.relres[c] = 0.0;
-      a.status[c] = 0;
-    }
-    cluster_barrier();   // no CTA leaves while another may still address it
-    return;
-  }
-  const double t2 = target * target;
-  const double t2lo = t2 * (1.0 - 4e-15), t2hi = t2 * (1.0 + 4e-15);
-
-  using Blk = std::conditional_t<ROT, SiteBlockRot<BX, BT>, SiteBlock<BX, BT>>;   // ROT: block_stencil.cuh
-  auto produce = [&](auto dag, double2* E, const Spinor* v) {
-    Blk::template produce<decltype(dag)::value>(u0, u1, v, [&](int plane, int idx, double2 val) {
-      constexpr int off[4] = {O0, O1, O2, O3};
-      E[off[plane] + idx * NT + tid] = val;
-    });
-  };
-  // interior: out = diag*v + the hops between this thread's own sites
-  // (register-only; runs between arrive and wait of the exchange barrier)
-  auto interior = [&](auto dag, const Spinor* v, Spinor* out) {
-    Blk::template interior<decltype(dag)::value>(u0, u1, v, out, a.diag);
-  };
-  // faces: add the hops exported by the neighbouring blocks (x-faces possibly
-  // from the neighbouring CTA's shared memory); all loads issued first
-  auto faces = [&](auto dag, const double2* E, uint32_t stage_off, Spinor* out) {
-    double2 fx[SPT], ft[SPT];
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const int i = k / BT, j = k % BT;
-      if (i == BX - 1) fx[k] = ld_dsmem(Xp + stage_off + 16u * (j * NT));
-      if (i == 0) fx[k] = ld_dsmem(Xm + stage_off + 16u * (j * NT));
-      if (j == BT - 1) ft[k] = E[O2 + i * NT + ttp];
-      if (j == 0) ft[k] = E[O3 + i * NT + ttm];
-    }
-    Blk::template faces<decltype(dag)::value>(u0, u1, fx, ft, out);
-  };
-  using F = std::integral_constant<bool, false>;
-  using T = std::integral_constant<bool, true>;
-
-  // out = D^dag D v (two exchange rounds).  Precondition: every CTA of the
-  // cluster has finished reading E0/E1 of the previous application.
-  auto normal_op = [&](const Spinor* v, Spinor* out) {
-    Spinor t[SPT];
-    produce(F{}, E0, v);
-    cluster_arrive();
-    interior(F{}, v, t);
-    cluster_wait();
-    faces(F{}, E0, 0u, t);
-    produce(T{}, E1, t);
-    cluster_arrive();
-    interior(T{}, t, out);
-    cluster_wait();
-    faces(T{}, E1, 16u * PL, out);
-  };
-
-  Spinor w[SPT];
-  double rs = normb2;   // r = b exactly: the same sum as ||b||^2 (fermion.py:186,191)
-  if (a.x0) {
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) x[k] = rot_in<ROT>(ldg_spinor(a.x0, cb + site(k)));
-    normal_op(x, w);
-    double rr = 0.0;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      r[k] = sp_sub(r[k], w[k]);
-      rr += spinor_norm2(r[k]);
-    }
-    publish(rr, 1);
-    cluster_barrier();
-    rs = total(1);
-  }
-#pragma unroll
-  for (int k = 0; k < SPT; ++k) p[k] = r[k];
-
-  double best = INFINITY;
-  double inv_rs = __drcp_rn(rs);
-  int it = 1;
-  int status = 1;
-  double relres = 0.0;
-  for (; it <= a.maxiter; ++it) {
-    // w = D^dag D p with <p, A p> = ||D p||^2 published by the stage barrier
-    Spinor t[SPT];
-    produce(F{}, E0, p);
-    cluster_arrive();
-    interior(F{}, p, t);
-    cluster_wait();
-    faces(F{}, E0, 0u, t);
-    double dd = 0.0;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) dd += spinor_norm2(t[k]);
-    produce(T{}, E1, t);
-    publish(dd, 0);
-    cluster_arrive();
-    interior(T{}, t, w);
-    cluster_wait();
-    faces(T{}, E1, 16u * PL, w);
-    const double den = total(0);
-    const double alpha = den > 0.0 ? rs / den : 0.0;
-    const bool repl = (it % kResReplace) == 0;
-    double rsn = 0.0;
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      if (!repl) {
-        r[k] = sp_fma(-alpha, w[k], r[k]);
-        rsn += spinor_norm2(r[k]);
-      }
-    }
-    double rs_new = 0.0;
-    bool check = true;
-    if (!repl) {
-      publish(rsn, 1);
-      cluster_arrive();
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) x[k] = sp_fma(alpha, p[k], x[k]);   // under the barrier
-      cluster_wait();
-      rs_new = total(1);
-      check = rs_new <= t2lo;
-      if (!check && rs_new <= t2hi) {
-        double sq;
-        asm volatile("sqrt.rn.f64 %0, %1;" : "=d"(sq) : "d"(rs_new));
-        check = sq <= target;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) x[k] = sp_fma(alpha, p[k], x[k]);
-    }
-    if (check) {   // true residual b - A x (shared with the residual replacement)
-      normal_op(x, w);
-      double tn2 = 0.0;
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) {
-        w[k] = sp_sub(rot_in<ROT>(ldg_spinor(a.b, cb + site(k))), w[k]);
-        tn2 += spinor_norm2(w[k]);
-      }
-      publish(tn2, 2);
-      cluster_barrier();
-      tn2 = total(2);
-      const double tn = sqrt(tn2);
-      if (!repl || tn <= target) best = tn / normb;
-      if (tn <= target) {
-        status = 0;
-        relres = tn / normb;
-        break;
-      }
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) r[k] = w[k];
-      rs_new = tn2;
-    }
-    double beta = 0.0;   // Markstein-finished rs'/rs (resident_col.cuh)
-    if (rs > 0.0) {
-      const double q0 = rs_new * inv_rs;
-      beta = __fma_rn(__fma_rn(-rs, q0, rs_new), inv_rs, q0);
-    }
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) p[k] = sp_fma(beta, p[k], r[k]);
-    rs = rs_new;
-    inv_rs = __drcp_rn(rs);
-  }
-#pragma unroll
-  for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(x[k]));
-  if (tid == 0 && rank == 0) {
-    a.iters[c] = status == 0 ? it : a.maxiter;
-    a.relres[c] = status == 0 ? relres : fmin(best, sqrt(rs) / normb);
-    a.status[c] = status;
-  }
-  cluster_barrier();   // no CTA leaves while another may still address its shared memory
-}
 
 // ---------------------------------------------------------------------------
-// k_cg_cluster_tx: the same solve without cluster-wide barriers.
+// k_cg_cluster_tx: no cluster-wide barrier inside the loop.
 //
 // The neighbouring CTAs' x-faces and every CTA's reduction partials are
 // PUSHED into the consumer's shared memory with st.async, each store

@@ -161,13 +161,3 @@ inline bool use_cg_while() {
   return v == 1;
 }
 
-// The streaming CG's stencil pass measured faster with the per-tile kernel
-// (profiles/r01/README.md); SCH_TMA_CG=1 switches it to the TMA pipeline.
-inline bool use_tma_cg() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SCH_TMA_CG");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1 && use_tma();
-}

@@ -268,31 +268,8 @@ struct TileShape {
   int tiles_x, tiles_t;
 };
 
-inline bool tma_tile_shape(int L, int T, int& TX);   // tma_tile.cuh
-inline bool use_tma();                                 // runtime.hpp
-
-// `tma`: the caller will run the TMA-pipelined stencil, so every pass of the
-// streaming CG must use its tiling for the per-tile partials to line up.
-inline TileShape pick_tile(int L, int T, bool tma = false) {
+inline TileShape pick_tile(int L, int T) {
   TileShape s;
-  int tx = 0;
-  if (tma && tma_tile_shape(L, T, tx)) {
-    if (T == 32 && tx == 16) return {1, 16, 32, L / 16, 1};
-    if (T == 32 && tx == 8) return {5, 8, 32, L / 8, 1};
-    if (T == 32 && tx == 4) return {8, 4, 32, L / 4, 1};
-    if (T == 16 && tx == 16) return {6, 16, 16, L / 16, 1};
-    if (T == 64 && tx == 4) return {7, 4, 64, L / 4, 1};
-  }
-  // tuning override for whole-row T = 32 tilings (SCH_CG_TILE = 1, 5, 9, 10, 11)
-  static int forced = -1;
-  if (forced < 0) {
-    const char* e = getenv("SCH_CG_TILE");
-    forced = e ? atoi(e) : 0;
-  }
-  if (T == 32 && forced > 0) {
-    const int txs = (forced == 5 || forced == 9) ? 8 : 16;
-    if (L % txs == 0) return {forced, txs, 32, L / txs, 1};
-  }
   if (L == 16 && T == 16) s = {0, 16, 16, 1, 1};
   else if (T == 32 && L % 16 == 0) s = {10, 16, 32, L / 16, 1};   // 256 thr, 3 CTAs/SM
   else if (T == 64 && L % 8 == 0) s = {2, 8, 64, L / 8, 1};
@@ -366,16 +343,9 @@ inline void launch_normal_tile(const TileShape& sh, const TileArgs& a, cudaStrea
                                int sparse_grid = 0, bool pdl = false) {
   switch (sh.kind) {
     case 0: launch_tile_inst<16, 16, 0, 0, MODE, 256, 3>(a, st, sparse_grid, pdl); break;
-    case 1: launch_tile_inst<16, 32, 2, 0, MODE, 512, 2>(a, st, sparse_grid, pdl); break;
     case 2: launch_tile_inst<8, 64, 2, 0, MODE, 512, 2>(a, st, sparse_grid, pdl); break;
     case 3: launch_tile_inst<16, 64, 2, 2, MODE, 512, 2>(a, st, sparse_grid, pdl); break;
-    case 5: launch_tile_inst<8, 32, 2, 0, MODE, 384, 2>(a, st, sparse_grid, pdl); break;
-    case 6: launch_tile_inst<16, 16, 2, 0, MODE, 320, 2>(a, st, sparse_grid, pdl); break;
-    case 7: launch_tile_inst<4, 64, 2, 0, MODE, 512, 2>(a, st, sparse_grid, pdl); break;
-    case 8: launch_tile_inst<4, 32, 2, 0, MODE, 256, 3>(a, st, sparse_grid, pdl); break;
-    case 9: launch_tile_inst<8, 32, 2, 0, MODE, 128, 4>(a, st, sparse_grid, pdl); break;
     case 10: launch_tile_inst<16, 32, 2, 0, MODE, 256, 3>(a, st, sparse_grid, pdl); break;
-    case 11: launch_tile_inst<16, 32, 2, 0, MODE, 128, 4>(a, st, sparse_grid, pdl); break;
     default: launch_tile_inst<8, 16, 2, 2, MODE, 128, 4>(a, st, sparse_grid, pdl); break;
   }
 }

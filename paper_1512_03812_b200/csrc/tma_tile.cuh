@@ -269,25 +269,12 @@ __global__ void __launch_bounds__(NT, MINB) k_normal_tma(TileArgs a) {
   }
 }
 
-// TMA tile configuration: SCH_TMA_CFG=<k> picks an entry of the table below
-// for T = 32 (tuning runs); the default is entry 0.
-inline int tma_cfg() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("SCH_TMA_CFG");
-    v = e ? atoi(e) : 6;   // measured best on cfg2 (profiles/r01/README.md)
-  }
-  return v;
-}
-
 // Host: shapes handled by the TMA path (whole time rows, x tiles of TX rows).
+// T = 32 (cfg2): 8 x 32 tiles, 128 threads, 2 stages, 3 CTAs/SM — measured
+// best of 16x32/512/1, 8x32/256/3, 4x32/256/3, 8x32/384/2, 8x32/192/3
+// (profiles/r01/README.md).
 inline bool tma_tile_shape(int L, int T, int& TX) {
-  if (T == 32) {
-    static const int tx_of_cfg[] = {8, 16, 8, 4, 8, 8, 8};
-    const int c = tma_cfg();
-    TX = tx_of_cfg[(c >= 0 && c < 7) ? c : 0];
-    return L % TX == 0;
-  }
+  if (T == 32 && L % 8 == 0) { TX = 8; return true; }
   if (T == 16 && L % 16 == 0) { TX = 16; return true; }
   if (T == 64 && L % 4 == 0) { TX = 4; return true; }
   return false;
@@ -311,7 +298,7 @@ inline int launch_tma_inst(const TileArgs& a, cudaStream_t st, int num_sms) {
 }
 
 // Launch the TMA-pipelined D^dag D for (L, T) if supported; returns false otherwise.
-//   T=32: 8 x 32 tiles, 384 threads, 2 CTAs/SM (cfg 0) | 16 x 32, 512 thr, 1 CTA/SM (cfg 1)
+//   T=32: 8 x 32 tiles (RX = 12), 128 threads, 3 CTAs/SM
 //   T=16: 16 x 16 tiles (RX = 20), 320 threads, 2 CTAs/SM
 //   T=64: 4 x 64 tiles (RX = 8), 512 threads, 2 CTAs/SM
 template <int MODE>
@@ -320,15 +307,7 @@ inline bool launch_normal_tma(const TileArgs& a, cudaStream_t st, int num_sms) {
   if (!tma_tile_shape(a.L, a.T, TX)) return false;
   constexpr int S = MODE == MODE_P ? 2 : 3;
   if (a.T == 32) {
-    switch (tma_cfg()) {
-      case 1: launch_tma_inst<16, 32, MODE, 512, S, 1>(a, st, num_sms); break;
-      case 2: launch_tma_inst<8, 32, MODE, 256, 2, 3>(a, st, num_sms); break;
-      case 3: launch_tma_inst<4, 32, MODE, 256, S, 3>(a, st, num_sms); break;
-      case 4: launch_tma_inst<8, 32, MODE, 384, 2, 2>(a, st, num_sms); break;
-      case 5: launch_tma_inst<8, 32, MODE, 192, 2, 3>(a, st, num_sms); break;
-      case 6: launch_tma_inst<8, 32, MODE, 128, 2, 3>(a, st, num_sms); break;
-      default: launch_tma_inst<8, 32, MODE, 384, S, 2>(a, st, num_sms); break;
-    }
+    launch_tma_inst<8, 32, MODE, 128, 2, 3>(a, st, num_sms);
   } else if (a.T == 16) {
     launch_tma_inst<16, 16, MODE, 320, S, 2>(a, st, num_sms);
   } else {
