@@ -144,3 +144,20 @@ def test_tune_acceptance_treats_cg_cap_as_rejection(experiment, monkeypatch):
     assert len(rows) == 1 + 2
     for r in rows[1:]:
         assert abs(float(r[8]) - 0.9) <= 0.02
+
+
+def test_load_setup_precedence(tmp_path):
+    """cli.py:32-46: defaults shrink to desk scale unless --paper-scale; the
+    experiment file replaces the defaults; --paper-scale, --seed and
+    --micro-ratio override either."""
+    from paper_1512_03812_b200.config import HmcConfig, desk_scale
+    cfg, plan = H.load_setup(None, None, False, None)
+    assert cfg == desk_scale(HmcConfig())
+    cfg, _ = H.load_setup(None, 7, True, 12.5)
+    assert (cfg.L, cfg.T, cfg.n_samples, cfg.seed, cfg.micro_ratio) == (32, 32, 200, 7, 12.5)
+    exp = tmp_path / "e.cfg"
+    exp.write_text("L = 8\nT = 8\nbeta = 1.5\nschemes = leapfrog\n")
+    cfg, plan = H.load_setup(str(exp), None, False, None)
+    assert (cfg.L, cfg.beta, plan.schemes) == (8, 1.5, ("leapfrog",))
+    cfg, _ = H.load_setup(str(exp), 3, True, None)
+    assert (cfg.L, cfg.beta, cfg.seed, cfg.n_samples) == (32, 1.5, 3, 200)
