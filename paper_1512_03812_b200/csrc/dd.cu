@@ -852,7 +852,8 @@ int sch_dd_create(sch_ctx* ctx, const void* nccl_id, int nranks, int rank, int L
       return sch_fail(ctx, SCH_ERR_CUDA, "dd_create: %s", cudaGetErrorString(e));
     }
   }
-  if (nranks > 1 && nccl_id != nullptr) {   // NCCL transport (else: p2p, connected later)
+  if (nccl_id != nullptr) {   // NCCL transport (else: local, or p2p connected later); one rank
+                              // is allowed: its faces go to itself by ncclSend/ncclRecv
     if (!nccl().ok) {
       delete dd;
       return sch_fail(ctx, SCH_ERR_CUDA, "libnccl.so.2 not available");

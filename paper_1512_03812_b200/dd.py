@@ -81,8 +81,11 @@ class StripLattice:
             transport = "nccl" if multi else "local"
         if transport not in TRANSPORTS:
             raise ValueError(f"unknown transport {transport!r}; valid: {', '.join(TRANSPORTS)}")
-        if transport == "nccl" and not multi:
-            raise ValueError("the NCCL transport needs a multi-rank process group")
+        if transport == "nccl" and not (multi or (group is None and strips is None
+                                                  and dist.is_initialized())):
+            raise ValueError("the NCCL transport needs a torch.distributed process group")
+        if transport == "nccl":
+            multi = True   # one strip per rank, even on a one-rank group
         if transport == "local" and multi:
             raise ValueError("the local transport keeps every strip in one process")
         self.transport = transport
@@ -95,7 +98,7 @@ class StripLattice:
             self.world, self.rank, self.local = 1, 0, int(strips or 1)
         ctx = _lib.ctx()
         nid = None
-        if self.world > 1 and transport == "nccl":
+        if transport == "nccl":
             buf = ctypes.create_string_buffer(128)
             if self.rank == 0:
                 ctx.call("sch_nccl_unique_id", ctypes.cast(buf, ctypes.c_void_p))

@@ -283,3 +283,51 @@ def test_dd_hmc_update_p2p_transport_matches_reference():
         assert abs(s.dh - so["dh"]) < 1e-8
         assert s.accepted == so["accepted"] and s.inversions == so["inversions"]
     assert np.max(np.abs(npy(lat.gather_links(q_ext)) - qo)) < 1e-8
+
+
+def test_dd_nccl_transport_on_one_rank_matches_local():
+    """The NCCL transport's code path (grouped ncclSend/ncclRecv of the faces
+    — here to the rank itself — ncclAllGather of the strip values, the
+    host-driven CG loop) on a one-rank process group: D^dag D, CG and a whole
+    HMC update bit-identical to the local transport.  (Across GPUs the pool
+    cannot run it: one GPU.)"""
+    import socket
+    import torch.distributed as dist
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice
+    from paper_1512_03812_b200.dd_hmc import dd_hmc_update
+    from oracle import schwinger_oracle as O
+    if dist.is_initialized():
+        pytest.skip("a process group is already initialised")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        L = 64
+        rng = np.random.default_rng(17)
+        q = rng.uniform(-np.pi, np.pi, (2, L, L))
+        psi = rng.standard_normal((L, L, 2)) + 1j * rng.standard_normal((L, L, 2))
+        lat_n = StripLattice(L, L, group=dist.group.WORLD, transport="nccl")
+        lat_l = StripLattice(L, L, strips=1)
+        assert lat_n.transport == "nccl" and (lat_n.world, lat_n.S) == (1, 1)
+        res = []
+        for lat in (lat_n, lat_l):
+            op = DDWilsonDirac(lat, lat.scatter_links(q), 0.1)
+            y = npy(lat.gather_spinor(op.normal(lat.scatter_spinor(psi))))
+            x, it, rel = op.cg(lat.scatter_spinor(psi), 1e-10)
+            res.append((y, npy(lat.gather_spinor(x)), it, rel))
+        assert np.array_equal(res[0][0], res[1][0])
+        assert np.array_equal(res[0][1], res[1][1]) and res[0][2:] == res[1][2:]
+        cfg = sw.HmcConfig(L=L, T=L, beta=2.0, m0=0.1, tau=0.5, h=0.25, scheme="adapted-nested-fg",
+                           micro_per_call=2, cg_tol=1e-10)
+        out = []
+        for lat in (lat_n, lat_l):
+            rng_h = O.make_rng(8, 0)
+            q0 = lat.scatter_links(O.hot_start(rng_h, L, L))
+            q1, st = dd_hmc_update(lat, q0, cfg, rng_h)
+            out.append((npy(lat.gather_links(q1)), st.dh, st.accepted, st.inversions))
+        assert np.array_equal(out[0][0], out[1][0]) and out[0][1:] == out[1][1:]
+    finally:
+        dist.destroy_process_group()
