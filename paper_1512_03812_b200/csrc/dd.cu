@@ -1029,9 +1029,9 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
     tx.bvec = (const double2*)b_ext;
     tx.out = r;
     tx.rowpart = part_b;
-    launch_dd_tile<MODE_X>(sh, tx, s);
+    if (!(t2d && launch_dd_tma2d<MODE_X>(tx, s, ctx->num_sms))) launch_dd_tile<MODE_X>(sh, tx, s);
     SCH_LAUNCHED(ctx);
-    if ((rc = dd_allsum(ctx, dd, part_b, st.sc + SC_RR))) return rc;
+    if ((rc = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, DDPost{}, t2d ? nch_p : 0))) return rc;
     if ((rc = dd_exchange(ctx, dd, (double*)r, 1, 4))) return rc;
     k_dd_copy<<<egrid, 256, 0, s>>>(r, p, nsites);
     SCH_LAUNCHED(ctx);
@@ -1078,11 +1078,12 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
       ctx->launches++;
       if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, post(POST_CHECK)))) break;
       // x halos are current (x is updated on every row), so no exchange here
-      launch_dd_tile<MODE_X>(sh, txx, q);
+      if (!(t2d && launch_dd_tma2d<MODE_X>(txx, q, ctx->num_sms))) launch_dd_tile<MODE_X>(sh, txx, q);
       ctx->launches++;
       // the final control also advances the iteration and, inside the WHILE
       // graph, sets the loop condition
-      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_TN2, post(POST_FINAL, h)))) break;
+      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_TN2, post(POST_FINAL, h), t2d ? nch_p : 0)))
+        break;
       cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) e = sch_fail(ctx, SCH_ERR_CUDA, "dd cg launch: %s", cudaGetErrorString(le));
     } while (0);

@@ -114,6 +114,9 @@ __global__ void __launch_bounds__(NT, MINB)
   const int per = a.tiles_x * a.tiles_t;
   const int ntiles = t.B * per;
   const int nown = t.own_hi - t.own_lo, nch = T / TT;
+  // the true-residual pass runs every CG iteration but has work only when the
+  // (global) stop test asked for it: exit before any load
+  if (MODE == MODE_X && t.flag != nullptr && t.flag[0] == 0) return;
   if (threadIdx.x == 0) {
     mbar_init(&bars[0], 1);
     mbar_init(&bars[1], 1);
@@ -328,9 +331,11 @@ inline bool tma2d_enabled() {
 // (two input spinor fields: 2 x 80 KB stages) with 16 x 32 tiles, 512
 // threads, 1 CTA/SM (0.334 vs 0.355 ms per CG iteration).  Smaller tiles at
 // 2 CTAs/SM, 8 x 32 at 1 CTA/SM with 128/448 threads, 12 x 32 and 4 x 32:
-// 0.337-0.425 ms.
+// 0.337-0.425 ms.  The true-residual pass (MODE_X, one input field + b read
+// at the output) takes the D^dag D's shape; when the stop test did not ask
+// for it, its CTAs exit before loading anything.
 template <int MODE>
 inline bool launch_dd_tma2d(const TileArgs& t, cudaStream_t st, int num_sms) {
-  if constexpr (MODE == MODE_PLAIN) return launch_dd_tma2d_inst<8, 32, MODE, 256, 1>(t, st, num_sms);
-  else return launch_dd_tma2d_inst<16, 32, MODE, 512, 1>(t, st, num_sms);
+  if constexpr (MODE == MODE_P) return launch_dd_tma2d_inst<16, 32, MODE, 512, 1>(t, st, num_sms);
+  else return launch_dd_tma2d_inst<8, 32, MODE, 256, 1>(t, st, num_sms);   // PLAIN, X: one field
 }
