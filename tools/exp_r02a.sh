@@ -1,4 +1,6 @@
 #!/bin/bash
+# Record of a round-2 experiment (profiles/r02/README.md).  Variant switches it sets
+# that lost their measurement were removed afterwards (the code is in git history).
 # round-2 kernel-variant experiment (run under gpurun): resident CG with x in
 # shared memory (SCH_RESBLK_XS), cluster CG shapes (SCH_CLUSTER), cluster
 # placement probe, parity of every variant against the default.

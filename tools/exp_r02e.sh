@@ -1,4 +1,6 @@
 #!/bin/bash
+# Record of a round-2 experiment (profiles/r02/README.md).  Variant switches it sets
+# that lost their measurement were removed afterwards (the code is in git history).
 # latency vs throughput of the resident / cluster CG: ns per chain-iteration
 # at B = one chain, one wave, many waves
 set -u

@@ -1,4 +1,6 @@
 #!/bin/bash
+# Record of a round-2 experiment (profiles/r02/README.md).  Variant switches it sets
+# that lost their measurement were removed afterwards (the code is in git history).
 set -u
 O=gpurun_out/exp_r02j
 mkdir -p $O

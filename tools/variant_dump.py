@@ -2,9 +2,12 @@
 batch under the current SCH_* kernel-variant environment, so that two
 variants can be compared bit for bit:
 
-    SCH_RESBLK_XS=6 python tools/variant_dump.py 16 2048 out_xs6.npz
+    SCH_RESBLK_ROT=0 python tools/variant_dump.py 16 2048 out_ref_basis.npz
     python tools/variant_dump.py 16 2048 out_base.npz
-    python tools/variant_dump.py --compare out_base.npz out_xs6.npz
+    python tools/variant_dump.py --compare out_base.npz out_ref_basis.npz
+
+(used in round 2 for the x-in-shared-memory, 8-CTA-cluster and mbarrier
+variants, all bit-identical to the default, profiles/r02/README.md)
 """
 import math
 import sys
