@@ -331,3 +331,31 @@ def test_dd_nccl_transport_on_one_rank_matches_local():
         assert np.array_equal(out[0][0], out[1][0]) and out[0][1:] == out[1][1:]
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scheme,G", [("adapted-nested-fg", 4), ("fg-approx", 2)])
+def test_dd_hmc_update_antiperiodic_matches_reference(scheme, G):
+    """Antiperiodic fermion boundary in time (BASELINE configs[0]; the sign
+    of U_t on the last time slice, applied per extended strip — strips cut
+    x, so every strip holds whole time rows): HMC updates on strips == the
+    oracle's antiperiodic hmc_update on the whole lattice."""
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200.dd import StripLattice
+    from paper_1512_03812_b200.dd_hmc import dd_hmc_update
+    from oracle import schwinger_oracle as O
+    L = 16
+    kw = dict(L=L, T=L, beta=2.0, m0=0.1, tau=1.0, h=0.25, scheme=scheme,
+              micro_per_call=2 if scheme.startswith(("nested", "adapted")) else None,
+              cg_tol=1e-10, fermion_bc="antiperiodic")
+    cfg, ocfg = sw.HmcConfig(**kw), O.Config(**kw)
+    lat = StripLattice(L, L, strips=G)
+    rng_g, rng_o = O.make_rng(12, 0), O.make_rng(12, 0)
+    q0 = O.hot_start(rng_g, L, L)
+    O.hot_start(rng_o, L, L)
+    q_ext, qo = lat.scatter_links(q0), q0
+    for _ in range(2):
+        q_ext, s = dd_hmc_update(lat, q_ext, cfg, rng_g)
+        qo, so = O.hmc_update(qo, ocfg, rng_o)
+        assert abs(s.dh - so["dh"]) < 1e-8
+        assert s.accepted == so["accepted"] and s.inversions == so["inversions"]
+    assert np.max(np.abs(npy(lat.gather_links(q_ext)) - qo)) < 1e-8

@@ -196,3 +196,26 @@ def test_parallel_oracle_equals_serial_oracle():
             qq, s = O.hmc_update(qq, O.Config(**kw), r)
             assert s["dh"] == ref[c][2][t] and s["accepted"] == ref[c][3][t]
         assert np.array_equal(qq, ref[c][1])
+
+
+@pytest.mark.parametrize("scheme,h,micro", [("adapted-nested-fg", 0.25, 2), ("5stage", 0.2, None)])
+def test_oracle_quenched_matches_reference(scheme, h, micro):
+    """Quenched updates (eta = 0, no pseudofermion draw; hmc.py:79-80)
+    against the reference's own run (tests/golden/make_quenched_golden.py)."""
+    from pathlib import Path
+    g = np.load(Path(__file__).resolve().parent / "golden" / "quenched.npz")
+    L = 12
+    cfg = O.Config(L=L, T=L, beta=2.0, m0=0.1, tau=1.0, h=h, scheme=scheme, micro_per_call=micro,
+                   cg_tol=1e-10, quenched=True)
+    rng = O.make_rng(5, 0)
+    q = O.hot_start(rng, L, L)
+    assert np.array_equal(q, g[f"{scheme}_q0"])
+    for k in range(3):
+        q, st = O.hmc_update(q, cfg, rng)
+        assert abs(st["dh"] - g[f"{scheme}_dh"][k]) < 1e-10
+        assert st["accepted"] == bool(g[f"{scheme}_acc"][k])
+        assert st["inversions"] == int(g[f"{scheme}_inv"][k])
+    assert np.max(np.abs(q - g[f"{scheme}_q"])) < 1e-10
+    m = O.measure_dh(g[f"{scheme}_q0"], cfg, O.make_rng(6, 1), 8)
+    assert np.max(np.abs(m["dh"] - g[f"{scheme}_mdh"])) < 1e-10
+    assert m["inversions_per_traj"] == int(g[f"{scheme}_minv"])
