@@ -427,3 +427,27 @@ def test_resident_cg_spin_basis_matches_reference_basis(tmp_path):
         a, b = res["0"][f"x{L}"], res["1"][f"x{L}"]
         assert rel_err(b, a) <= TOL_OP, (L, rel_err(b, a))
         np.testing.assert_array_equal(res["0"][f"it{L}"], res["1"][f"it{L}"])
+
+
+def test_thermalize_matches_reference(sw):
+    """thermalize (hmc.py:133-155): cold start, 60 leapfrog updates with the
+    reference's step annealing (it fires once: 0.1 -> 0.07) at the paper's
+    mass on 8x8, against the reference's own run (tests/golden/therm.npz)."""
+    from pathlib import Path
+    g = np.load(Path(__file__).resolve().parent / "golden" / "therm.npz")
+    cfg = sw.HmcConfig(L=8, T=8, beta=1.0, m0=-0.231367, tau=1.0, h=0.1, cg_tol=1e-10,
+                       n_thermalize=60, seed=11)
+    q, hist = sw.thermalize(cfg, sw.make_rng(11, 0))
+    hist, ref = np.asarray(hist), g["history"]
+    # the same accept/reject sequence (a rejection repeats the plaquette) and
+    # so the same annealing; the chains agree to rounding at first, and at
+    # this light mass the molecular dynamics amplify the rounding-level
+    # difference of each trajectory (1e-13 -> ~1e-11 after 5 updates ->
+    # ~1e-6 after 60, measured), as between any two float64 implementations
+    assert np.array_equal(np.diff(hist) == 0, np.diff(ref) == 0)
+    assert np.max(np.abs(hist[:5] - ref[:5])) < 1e-10
+    assert np.max(np.abs(hist - ref)) < 1e-4
+    assert np.max(np.abs(q.cpu().numpy() - g["q"])) < 1e-3
+    from dataclasses import replace
+    q5, _ = sw.thermalize(replace(cfg, n_thermalize=5), sw.make_rng(11, 0))
+    assert np.max(np.abs(q5.cpu().numpy() - g["q5"])) < 1e-9

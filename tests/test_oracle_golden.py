@@ -219,3 +219,15 @@ def test_oracle_quenched_matches_reference(scheme, h, micro):
     m = O.measure_dh(g[f"{scheme}_q0"], cfg, O.make_rng(6, 1), 8)
     assert np.max(np.abs(m["dh"] - g[f"{scheme}_mdh"])) < 1e-10
     assert m["inversions_per_traj"] == int(g[f"{scheme}_minv"])
+
+
+def test_oracle_thermalize_matches_reference():
+    """thermalize (hmc.py:133-155) against the reference's own 60-update run
+    with one step annealing (tests/golden/make_therm_golden.py)."""
+    from pathlib import Path
+    g = np.load(Path(__file__).resolve().parent / "golden" / "therm.npz")
+    cfg = O.Config(L=8, T=8, beta=1.0, m0=-0.231367, tau=1.0, h=0.1, cg_tol=1e-10,
+                   n_thermalize=60, seed=11)
+    q, hist = O.thermalize(cfg, O.make_rng(11, 0))
+    assert np.max(np.abs(np.asarray(hist) - g["history"])) < 1e-10   # same NumPy arithmetic
+    assert np.max(np.abs(q - g["q"])) < 1e-8
