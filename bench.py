@@ -119,6 +119,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-compare", action="store_true",
                     help="skip the cfg3 integrator comparison (five schemes at ~90%% acceptance)")
+    ap.add_argument("--graph", choices=("auto", "on", "off"), default="auto",
+                    help="replay each ensemble update as one captured CUDA graph (auto: when "
+                         "a GPU holds <= 2048 chains, the strong-scaled shares at 4-8 GPUs)")
     ap.add_argument("--streams", type=int, default=1,
                     help="sub-ensembles issued concurrently on separate streams (measured "
                          "slower than 1 on cfg3: 2 -> -6 %%, profiles/r01/README.md)")
@@ -823,6 +826,48 @@ def run_ours(args):
     sts = run_steps(args.therm + args.warmup)
     torch.cuda.synchronize()
 
+    # Small per-GPU ensembles (the strong-scaled shares at 4-8 GPUs): one
+    # captured CUDA graph per update (EnsembleUpdateGraph) instead of ~100
+    # launches issued from Python — measured 6.92 -> 6.49 ms per update at
+    # 1024 chains (tools/graph_vs_eager.py).  The CG launches' events inside
+    # the graph are external event nodes, so the roofline below reads the CG
+    # time and iterations of the last timed replay.
+    mega_on = args.workload == "cfg3" and sw.hmc._mega_eligible(cfg, True)
+    use_graph = S == 1 and not mega_on and (
+        args.graph == "on" or (args.graph == "auto" and chains <= 2048))
+    upd = graph_prof = None
+    if use_graph:
+        graph_prof = []
+        upd = sw.EnsembleUpdateGraph(qs[0], cfg, drngs[0], cg_profile=graph_prof)
+        upd.step()
+        upd.stats()          # one untimed replay
+        torch.cuda.synchronize()
+
+    def run_graph_steps(n, on_stats=None, ahead=2):
+        """run_steps for the graph: each replay's per-chain dH / accept copied
+        out (the graph's buffers are rewritten by the next replay) and read
+        back `ahead` replays later."""
+        from types import SimpleNamespace
+        queue, sts = [], None
+
+        def resolve(item):
+            dh, acc = item[0].cpu().numpy(), item[1].cpu().numpy()
+            if (acc < 0).any():
+                raise ValueError(f"non-finite energy change {dh[acc < 0][0]}")
+            return [SimpleNamespace(dh=dh, accepted=acc == 1, inversions=upd.inversions)]
+        for _ in range(n):
+            dh, acc = upd.step()
+            queue.append((dh.clone(), acc.clone()))
+            if len(queue) > ahead:
+                sts = resolve(queue.pop(0))
+                if on_stats:
+                    on_stats(sts)
+        while queue:
+            sts = resolve(queue.pop(0))
+            if on_stats:
+                on_stats(sts)
+        return sts
+
     clocks = ClockSampler(local)
     # nvidia-smi's own start-up (NVML init) contends with this process's
     # launches: start it before the timed region and keep only its samples
@@ -841,15 +886,22 @@ def run_ours(args):
         acc.append(np.concatenate([st.accepted for st in sts]))
         dhs.append(np.concatenate([st.dh for st in sts]))
 
-    sts = run_steps(args.steps, record)
+    sts = run_graph_steps(args.steps, record) if use_graph else run_steps(args.steps, record)
     st = sts[0]
     e1.record()
     torch.cuda.synchronize()
     barrier()
     launches = _lib.launch_count() - launches0
+    if use_graph:   # replays launch no kernels from the host: count the captured ones
+        upd.stats()   # CG-cap / non-finite check of the last replay
+        launches = upd.launches_per_replay * args.steps
+        qs[0] = upd.q.clone()
     clocks.mark(t_wall0, time.time())
     clk = clocks.stop()
     prof, F.CG_PROFILE = F.CG_PROFILE, None
+    prof_steps = 1 if use_graph else args.steps   # steps the CG events / iteration counts cover
+    if use_graph:
+        prof = graph_prof
     ms = e0.elapsed_time(e1)
     if world > 1:
         ms = _max_over_ranks(dist, torch, ms)
@@ -871,8 +923,11 @@ def run_ours(args):
     if cur is not None:
         cg_ms += cur[1] - cur[0]
     cg_iters = sum(int(it.sum().item()) for _, _, it, _ in prof)
+    if prof_steps != args.steps:   # graph: the last replay stands for every timed step
+        scale = args.steps / prof_steps
+        cg_ms, cg_iters = cg_ms * scale, int(round(cg_iters * scale))
     V = cfg.L * cfg.T
-    n_solves = len(prof)
+    n_solves = len(prof) * (args.steps // prof_steps)   # CG launches in the timed region
     mega = args.workload == "cfg3" and sw.hmc._mega_eligible(cfg, True)
     kinfo = CG_KERNELS["cfg3_mega" if mega else args.workload]
     cg_bytes = 352.0 * V * cg_iters
@@ -1001,7 +1056,11 @@ def run_ours(args):
                        "inversions_per_traj_reference_convention": st.inversions,
                        "cg_iterations_per_chain_traj": cg_iters / (chains * args.steps),
                        "cg_iterations_per_solve": cg_iters / max(1, chains * n_solves),
-                       "therm_updates_before_warmup": args.therm},
+                       "therm_updates_before_warmup": args.therm,
+                       "update_issue": ("one CUDA-graph replay per update; the CG time and "
+                                        "iterations are the last timed replay's (external "
+                                        "event nodes) x steps") if use_graph else
+                                       "eager, two updates queued ahead"},
             "roofline": {"bound": "fp64", "achieved": fp64_achieved, "peak": fp64_peak,
                          "unit": "TFLOP/s", "frac": fp64_achieved / fp64_peak,
                          "traffic": (None if kinfo["dram_per_site"] is None

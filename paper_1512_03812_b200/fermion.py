@@ -235,8 +235,16 @@ def spinor_norm(a) -> torch.Tensor:
 
 # When set to a list, every cg_solve appends (start_event, end_event,
 # iters_tensor, sites_per_chain) so a benchmark can time the CG kernels on
-# their own stream and count the iterations they ran.
+# their own stream and count the iterations they ran.  Inside a CUDA-graph
+# capture the events are external event-record nodes: after each replay
+# they hold that replay's timestamps (and the iteration tensors its counts).
 CG_PROFILE: list | None = None
+
+
+def _profile_events():
+    ext = torch.cuda.is_current_stream_capturing()
+    return (torch.cuda.Event(enable_timing=True, external=ext),
+            torch.cuda.Event(enable_timing=True, external=ext))
 
 
 def cg_solve(op: WilsonDirac, b, tol: float, maxiter: int = DEFAULT_MAXITER, x0=None,
@@ -254,7 +262,7 @@ def cg_solve(op: WilsonDirac, b, tol: float, maxiter: int = DEFAULT_MAXITER, x0=
     status = torch.empty((B,), dtype=torch.int32, device=dev)
     prof = CG_PROFILE
     if prof is not None:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0, ev1 = _profile_events()
         ev0.record()
     _lib.ctx().call("sch_cg_normal", _lib.ptr(U), _lib.ptr(b), _lib.ptr(x), _lib.ptr(x0), B, op.L,
                     op.T, op.m0, float(tol), int(maxiter), STOP_MODES[stop], _lib.ptr(iters),
@@ -383,7 +391,7 @@ def _solve_apply(op: WilsonDirac, b, tol: float, maxiter: int, x0, stop: str):
     status = torch.empty((B,), dtype=torch.int32, device=dev)
     prof = CG_PROFILE
     if prof is not None:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0, ev1 = _profile_events()
         ev0.record()
     _lib.ctx().call("sch_chi_xi", _lib.ptr(U), _lib.ptr(b), _lib.ptr(dx), _lib.ptr(x),
                     _lib.ptr(x0), B, op.L, op.T, op.m0, float(tol), int(maxiter),

@@ -409,7 +409,8 @@ class EnsembleUpdateGraph:
     resident or cluster-resident CG engines (V <= 1024, or 64^2): the
     streaming engine runs its own device-side graph."""
 
-    def __init__(self, q, config: HmcConfig, device_rng: NumpyDeviceRng, reuse_solves: bool = True):
+    def __init__(self, q, config: HmcConfig, device_rng: NumpyDeviceRng, reuse_solves: bool = True,
+                 cg_profile: list | None = None):
         if not isinstance(device_rng, NumpyDeviceRng):
             raise TypeError("graph capture needs the device-resident NumpyDeviceRng streams")
         V = config.L * config.T
@@ -428,9 +429,19 @@ class EnsembleUpdateGraph:
         device_rng.state.copy_(saved)            # the warm-up's draws are given back
         self.graph = torch.cuda.CUDAGraph()
         counter = InversionCounter()
-        with torch.cuda.graph(self.graph, stream=self._stream):
-            out, pend = hmc_update_ensemble_async(self.q, config, device_rng, counter, reuse_solves)
-            self.q.copy_(out)
+        # cg_profile: the CG launches' events and iteration tensors of the
+        # captured update (external event nodes: each replay refreshes them)
+        from . import fermion as _fermion
+        saved_prof, _fermion.CG_PROFILE = _fermion.CG_PROFILE, cg_profile
+        launches0 = _lib.launch_count()
+        try:
+            with torch.cuda.graph(self.graph, stream=self._stream):
+                out, pend = hmc_update_ensemble_async(self.q, config, device_rng, counter,
+                                                      reuse_solves)
+                self.q.copy_(out)
+        finally:
+            _fermion.CG_PROFILE = saved_prof
+        self.launches_per_replay = _lib.launch_count() - launches0   # our kernels in the graph
         self._pending = pend
         self._infos = list(pend._state._infos)
         self.inversions = pend._result.inversions
