@@ -852,12 +852,14 @@ def run_ours(args):
 
         def resolve(item):
             dh, acc = item[0].cpu().numpy(), item[1].cpu().numpy()
+            if int(item[2].item()):
+                raise F.SolverError("a CG solve of the replayed update hit its cap", float("nan"))
             if (acc < 0).any():
                 raise ValueError(f"non-finite energy change {dh[acc < 0][0]}")
             return [SimpleNamespace(dh=dh, accepted=acc == 1, inversions=upd.inversions)]
         for _ in range(n):
             dh, acc = upd.step()
-            queue.append((dh.clone(), acc.clone()))
+            queue.append((dh.clone(), acc.clone(), upd.failed.clone()))
             if len(queue) > ahead:
                 sts = resolve(queue.pop(0))
                 if on_stats:

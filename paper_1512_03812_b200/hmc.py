@@ -439,6 +439,10 @@ class EnsembleUpdateGraph:
                 out, pend = hmc_update_ensemble_async(self.q, config, device_rng, counter,
                                                       reuse_solves)
                 self.q.copy_(out)
+                # any CG of this replay at its cap (0/1), formed inside the graph
+                flags = [i.status_dev.reshape(-1) for i in pend._state._infos]
+                self.failed = (torch.cat(flags).amax() if flags
+                               else torch.zeros((), dtype=torch.int32, device=self.q.device))
         finally:
             _fermion.CG_PROFILE = saved_prof
         self.launches_per_replay = _lib.launch_count() - launches0   # our kernels in the graph
@@ -450,7 +454,8 @@ class EnsembleUpdateGraph:
 
     def step(self):
         """Replay one update on the current stream; returns the pending
-        per-chain (dH, accept) tensors (read them with ``stats()``)."""
+        per-chain (dH, accept) tensors (read them with ``stats()``;
+        ``self.failed`` is 1 when a CG solve of the replay hit its cap)."""
         self.graph.replay()
         return self._pending.dh_dev, self._pending.acc_dev
 
