@@ -120,8 +120,9 @@ def parse():
     ap.add_argument("--no-compare", action="store_true",
                     help="skip the cfg3 integrator comparison (five schemes at ~90%% acceptance)")
     ap.add_argument("--graph", choices=("auto", "on", "off"), default="auto",
-                    help="replay each ensemble update as one captured CUDA graph (auto: when "
-                         "a GPU holds <= 2048 chains, the strong-scaled shares at 4-8 GPUs)")
+                    help="replay each ensemble update as one captured CUDA graph (auto/on: "
+                         "whenever one stream issues the ensemble and the megakernel is off; "
+                         "off: eager issue, two updates queued ahead)")
     ap.add_argument("--streams", type=int, default=1,
                     help="sub-ensembles issued concurrently on separate streams (measured "
                          "slower than 1 on cfg3: 2 -> -6 %%, profiles/r01/README.md)")
@@ -826,15 +827,14 @@ def run_ours(args):
     sts = run_steps(args.therm + args.warmup)
     torch.cuda.synchronize()
 
-    # Small per-GPU ensembles (the strong-scaled shares at 4-8 GPUs): one
-    # captured CUDA graph per update (EnsembleUpdateGraph) instead of ~100
-    # launches issued from Python — measured 6.92 -> 6.49 ms per update at
-    # 1024 chains (tools/graph_vs_eager.py).  The CG launches' events inside
-    # the graph are external event nodes, so the roofline below reads the CG
-    # time and iterations of the last timed replay.
+    # One captured CUDA graph per update (EnsembleUpdateGraph) instead of
+    # ~100 launches issued from Python: 1024 chains (the 8-GPU share) 141-142k
+    # -> 152-154k chain-traj/s, 8192 chains 192.6-192.8k -> 194.0-194.2k, and
+    # host stalls no longer reach the GPU (profiles/r02/README.md).  The CG
+    # launches' events inside the graph are external event nodes, so the
+    # roofline below reads the CG time and iterations of the last timed replay.
     mega_on = args.workload == "cfg3" and sw.hmc._mega_eligible(cfg, True)
-    use_graph = S == 1 and not mega_on and (
-        args.graph == "on" or (args.graph == "auto" and chains <= 2048))
+    use_graph = S == 1 and not mega_on and args.graph in ("auto", "on")
     upd = graph_prof = None
     if use_graph:
         graph_prof = []
