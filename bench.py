@@ -950,7 +950,79 @@ def run_ours(args):
 
     # e2e through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and use_graph:
+        # The same contract with the update as graph replays (public API:
+        # EnsembleUpdateGraph): two captured graphs, one per in-flight step,
+        # each with its own link buffer (they share the chains' RNG state).
+        # Step k uploads the host links into graph k%2's buffer on a copy
+        # stream, replays it, and downloads its new links and per-chain
+        # dH / accept into pinned host memory; the host reads step k-1's
+        # after issuing step k.
+        q_host = qs[0].cpu().pin_memory()
+        q_back = torch.empty_like(q_host).pin_memory()
+        h2d = q_host.numel() * 8
+        steps_e2e = max(4, args.steps)
+        upds = [upd] + [sw.EnsembleUpdateGraph(qs[0], cfg, drngs[0])]
+        dh_host = [torch.empty((chains,), dtype=torch.float64).pin_memory() for _ in range(2)]
+        acc_host = [torch.empty((chains,), dtype=torch.int32).pin_memory() for _ in range(2)]
+        fail_host = [torch.empty((), dtype=torch.int32).pin_memory() for _ in range(2)]
+        cp = torch.cuda.Stream()
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]   # slot's results downloaded
+        ev_done = [torch.cuda.Event() for _ in range(2)]
+        for slot in range(2):
+            ev_out[slot].record(main)
+        barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record()
+        cp.wait_stream(main)
+
+        def upload(slot):
+            with torch.cuda.stream(cp):
+                cp.wait_event(ev_out[slot])   # the slot's previous step is downloaded
+                upds[slot].q.copy_(q_host, non_blocking=True)
+                ev_in[slot].record(cp)
+
+        def read(k):
+            slot = k % 2
+            ev_out[slot].synchronize()
+            if int(fail_host[slot].item()):
+                raise F.SolverError("a CG solve of the replayed update hit its cap", float("nan"))
+            if (acc_host[slot].numpy() < 0).any():
+                raise ValueError("non-finite energy change")
+
+        upload(0)
+        for k in range(steps_e2e):
+            slot = k % 2
+            if k + 1 < steps_e2e:
+                upload(1 - slot)
+            main.wait_event(ev_in[slot])
+            dh_dev, acc_dev = upds[slot].step()
+            ev_done[slot].record(main)
+            with torch.cuda.stream(cp):
+                cp.wait_event(ev_done[slot])
+                q_back.copy_(upds[slot].q, non_blocking=True)
+                dh_host[slot].copy_(dh_dev, non_blocking=True)
+                acc_host[slot].copy_(acc_dev, non_blocking=True)
+                fail_host[slot].copy_(upds[slot].failed, non_blocking=True)
+                ev_out[slot].record(cp)
+            if k >= 1:   # step k-1's dH / accept (its slot is not rewritten before
+                read(k - 1)   # step k+1 is issued), read while step k is queued
+        read(steps_e2e - 1)
+        main.wait_stream(cp)
+        f1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ems = f0.elapsed_time(f1)
+        if world > 1:
+            ems = _max_over_ranks(dist, torch, ems)
+        d2h = q_back.numel() * 8 + chains * (8 + 4)
+        e2e = {"value": shard.total / (ems / steps_e2e * 1e-3), "unit": "chain-trajectories/s",
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": ems / steps_e2e,
+               "issue": "EnsembleUpdateGraph replays, host links in / out every step"}
+    elif not args.no_e2e:
         # Every step is one public-API call on HOST links: H2D of the links,
         # the update, D2H of the new links and of the per-chain dH / accept.
         # Copies run on a copy stream, double-buffered, so step k+1's upload
