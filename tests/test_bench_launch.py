@@ -62,3 +62,30 @@ def test_gpus_2_ensemble_bench_splits_the_chains(weak):
     assert line["config"]["global_chains"] == (128 if weak else 64)
     assert line["config"]["chains_per_gpu"] == (64 if weak else 32)
     assert line["value"] > 0 and line["roofline"]["bound"] == "fp64"
+
+
+@pytest.mark.gpu
+def test_bench_line_contract():
+    """The single-GPU bench line carries every key of the driver's contract
+    (bench.py docstring / task contract): metric, value, unit, n_gpus,
+    steps, warmup, ms_per_step, higher_is_better, scaling, vs_baseline,
+    dtype, data, config.workload, roofline {bound, achieved, peak, unit,
+    frac, traffic}, e2e {value, unit, h2d/d2h bytes}, gpu_launches, clocks."""
+    r = _run(["--steps", "3", "--warmup", "3", "--no-cpu", "--no-stencil", "--no-compare"])
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = _line(r.stdout)
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config", "roofline",
+              "e2e", "gpu_launches", "clocks"):
+        assert k in line, k
+    assert line["n_gpus"] == 1 and line["steps"] == 3 and line["warmup"] == 3
+    assert line["value"] > 0 and line["higher_is_better"] is True
+    assert "workload" in line["config"]
+    roof = line["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in roof, k
+    assert abs(roof["frac"] - roof["achieved"] / roof["peak"]) < 1e-9
+    e2e = line["e2e"]
+    assert e2e["value"] > 0 and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
+    assert line["gpu_launches"] > 0
+    assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(line["clocks"])
