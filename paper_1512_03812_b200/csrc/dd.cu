@@ -53,6 +53,7 @@
 #include "runtime.hpp"
 #include "tile.cuh"
 #include "tma2d.cuh"
+#include "march.cuh"
 #include "tma_tile.cuh"
 #include "../../include/schwinger_sm100.h"
 
@@ -421,6 +422,34 @@ __global__ void k_p2p_pull(double* __restrict__ f, int P, int W, P2PArgs a) {
 // global memory by one warp: lane l owns [l*K, l*K + K), K = the power of two
 // >= n/32; every lane returns the sum.
 SCH_DEV double warp_canon(const double* v, int n, int lane) {
+  if (n > 64 && (n & 1) == 0) {
+    // long rows (the marching pass writes T/4 partials per row): coalesced
+    // 16-B loads, chunk by chunk.  Lane l of chunk c holds values 64c + 2l,
+    // 64c + 2l + 1: their sum is the tree's first level, the xor butterfly
+    // the next five, so every lane ends with the subtree of the aligned
+    // 64-chunk; lane c keeps chunk c's value and the butterfly over the lanes
+    // (zero padded) is the top of the tree.  n <= 2048.
+    double keep = 0.0;
+    const int nc = (n + 63) / 64;
+    for (int c0 = 0; c0 < nc; c0 += 4) {
+      double a[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = 64 * (c0 + j) + 2 * lane;
+        a[j] = 0.0;
+        if (i < n) {
+          const double2 q = __ldcg(reinterpret_cast<const double2*>(v + i));
+          a[j] = q.x + q.y;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        a[j] = warp_tree_sum(a[j]);
+        if (lane == c0 + j) keep = a[j];
+      }
+    }
+    return warp_tree_sum(keep);
+  }
   int K = 1;
   while (32 * K < n) K <<= 1;
   double a[8];
@@ -508,6 +537,7 @@ struct RowRed {
   const double* part;   // [S][Lloc][nch] row-chunk partials
   int S, Lloc, nch, nb; // nb = ceil(Lloc / kRowBlk)
   double* blk;          // [S][nb]
+  const int* need;      // when set and need[0] == 0 the sum is not used: nothing is read
   int* ctr;             // last-CTA ticket (reset by the last CTA)
   int mode;
   double* out;          // local: the global sum; NCCL: this rank's strip value
@@ -542,11 +572,21 @@ __global__ void __launch_bounds__(256) k_dd_rowred(RowRed a) {
   __shared__ int last;
   const int b = blockIdx.x, s = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // The true-residual sum of an iteration whose stop test did not ask for it
+  // (its pass wrote nothing, dd_final ignores the value; `need` is the same
+  // on every rank, and is rewritten only by the post of this kernel's last
+  // CTA, after every CTA has read it).  Local transport: only the control
+  // runs; the others keep their protocol and push zeros.
+  const bool skip = a.need != nullptr && a.need[0] == 0;
+  if (skip && a.mode == RED_LOCAL) {
+    if (b == 0 && s == 0 && threadIdx.x == 0) dd_post_run(a.post);
+    return;
+  }
   constexpr int RPW = kRowBlk / 8;   // rows per warp (8 warps)
   for (int i = 0; i < RPW; ++i) {
     const int y = b * kRowBlk + warp * RPW + i;
     double v = 0.0;
-    if (y < a.Lloc) v = warp_canon(a.part + ((long long)s * a.Lloc + y) * a.nch, a.nch, lane);
+    if (y < a.Lloc && !skip) v = warp_canon(a.part + ((long long)s * a.Lloc + y) * a.nch, a.nch, lane);
     if (lane == 0) rv[warp * RPW + i] = v;
   }
   __syncthreads();
@@ -601,7 +641,7 @@ __global__ void k_dd_tree_post(const double* __restrict__ vals, int G, double* _
 // the global sum of the row partials `part` ([S][Lloc][NC]) into *out (on
 // the device, every rank); `post` runs on the sum
 int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, double* out,
-              const DDPost& post = DDPost{}, int nch = 0) {
+              const DDPost& post = DDPost{}, int nch = 0, const int* need = nullptr) {
   if (!dd->p2p && dd->comm == nullptr && dd->nranks > 1)
     return sch_fail(ctx, SCH_ERR_ARG, "dd: no transport (NCCL id or p2p connect)");
   RowRed a;
@@ -611,6 +651,7 @@ int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, double* out,
   a.nch = nch > 0 ? nch : dd->NC;   // chunks per row of `part` (any power-of-two width: same tree)
   a.nb = (dd->Lloc + kRowBlk - 1) / kRowBlk;
   a.blk = dd->red_blk;
+  a.need = need;
   a.ctr = dd->red_ctr;
   a.mode = dd->p2p ? RED_P2P : dd->comm ? RED_NCCL : RED_LOCAL;
   a.out = a.mode == RED_NCCL ? dd->red_all : out;
@@ -782,6 +823,26 @@ inline unsigned chunk_grid(long long items) {
 // stencil pass (T a multiple of 32); SCH_DD_TMA2D=0 keeps the
 // one-tile-per-CTA halo kernel
 bool dd_use_tma2d(const sch_dd* dd) { return tma2d_enabled() && tma2d_shape_ok(dd->Lloc, dd->T); }
+
+// The stencil pass of the decomposed lattice: the warp-marching register
+// kernel (march.cuh; SCH_DD_MARCH=0 turns it off), else the TMA 2-D tile
+// kernel (T a multiple of 32), else the one-tile-per-CTA halo kernel.  All
+// three write canonical row-chunk partials; only the chunk width differs.
+enum { ST_TILE = 0, ST_TMA2D = 1, ST_MARCH = 2 };
+int dd_stencil_kind(const sch_dd* dd) {
+  if (march_enabled() && march_shape_ok(dd->T)) return ST_MARCH;
+  return dd_use_tma2d(dd) ? ST_TMA2D : ST_TILE;
+}
+// chunks per row of the stencil pass's partials (0: the lattice's own NC)
+int dd_stencil_nch(const sch_dd* dd, int kind) {
+  return kind == ST_MARCH ? march_nch(dd->T) : kind == ST_TMA2D ? dd->T / kT2T : 0;
+}
+template <int MODE>
+void dd_stencil_launch(int kind, const TileShape& sh, const TileArgs& a, cudaStream_t st, int num_sms) {
+  if (kind == ST_MARCH && launch_dd_march<MODE>(a, st, num_sms)) return;
+  if (kind == ST_TMA2D && launch_dd_tma2d<MODE>(a, st, num_sms)) return;
+  launch_dd_tile<MODE>(sh, a, st);
+}
 
 TileArgs dd_tile_args(sch_dd* dd, const TileShape& sh, const double2* U, double m0) {
   TileArgs a{};
@@ -971,8 +1032,7 @@ int sch_dd_ddagd(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* psi_ext,
   TileArgs a = dd_tile_args(dd, sh, (const double2*)U_ext, m0);
   a.in = (const double2*)psi_ext;
   a.out = (double2*)out_ext;
-  if (!(dd_use_tma2d(dd) && launch_dd_tma2d<MODE_PLAIN>(a, ctx->stream, ctx->num_sms)))
-    launch_dd_tile<MODE_PLAIN>(sh, a, ctx->stream);
+  dd_stencil_launch<MODE_PLAIN>(dd_stencil_kind(dd), sh, a, ctx->stream, ctx->num_sms);
   SCH_LAUNCHED(ctx);
   return SCH_OK;
 }
@@ -987,8 +1047,9 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   dd_tile_shape(dd->Lext, dd->T, sh);
   const long long nsites = (long long)dd->S * dd->Lext * dd->T;
   const size_t vec = (size_t)nsites * 2 * sizeof(double2);
-  const bool t2d = dd_use_tma2d(dd);
-  const int nch_p = t2d ? dd->T / kT2T : dd->NC;            // chunks per row of the stencil pass
+  const int skind = dd_stencil_kind(dd);
+  const int nch_s = dd_stencil_nch(dd, skind);              // chunks per row of the stencil pass (0: NC)
+  const int nch_p = nch_s ? nch_s : dd->NC;
   const size_t npart = (size_t)dd->S * dd->Lloc * std::max(dd->NC, nch_p);   // row partials
   const size_t bytes = 3 * vec + sizeof(double) * (2 * npart + SC_COUNT + dd->S + 64) +
                        sizeof(int) * (dd->S + 8) + 8 * 256;
@@ -1029,9 +1090,9 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
     tx.bvec = (const double2*)b_ext;
     tx.out = r;
     tx.rowpart = part_b;
-    if (!(t2d && launch_dd_tma2d<MODE_X>(tx, s, ctx->num_sms))) launch_dd_tile<MODE_X>(sh, tx, s);
+    dd_stencil_launch<MODE_X>(skind, sh, tx, s, ctx->num_sms);
     SCH_LAUNCHED(ctx);
-    if ((rc = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, DDPost{}, t2d ? nch_p : 0))) return rc;
+    if ((rc = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, DDPost{}, nch_s))) return rc;
     if ((rc = dd_exchange(ctx, dd, (double*)r, 1, 4))) return rc;
     k_dd_copy<<<egrid, 256, 0, s>>>(r, p, nsites);
     SCH_LAUNCHED(ctx);
@@ -1070,19 +1131,19 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
     int e = SCH_OK;
     do {
       if ((e = dd_exchange(ctx, dd, (double*)r, 1, 4))) break;
-      if (!(t2d && launch_dd_tma2d<MODE_P>(tp, q, ctx->num_sms))) launch_dd_tile<MODE_P>(sh, tp, q);
+      dd_stencil_launch<MODE_P>(skind, sh, tp, q, ctx->num_sms);
       ctx->launches++;
-      if ((e = dd_allsum(ctx, dd, part_a, st.sc + SC_PAP, post(POST_ALPHA), t2d ? nch_p : 0))) break;
+      if ((e = dd_allsum(ctx, dd, part_a, st.sc + SC_PAP, post(POST_ALPHA), nch_s))) break;
       k_dd_update<<<egrid, 256, 0, q>>>(r, p, (double2*)x_ext, ap, st, dd->S, dd->Lext, dd->T, dd->CW,
                                         lo, hi, part_b);
       ctx->launches++;
       if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, post(POST_CHECK)))) break;
       // x halos are current (x is updated on every row), so no exchange here
-      if (!(t2d && launch_dd_tma2d<MODE_X>(txx, q, ctx->num_sms))) launch_dd_tile<MODE_X>(sh, txx, q);
+      dd_stencil_launch<MODE_X>(skind, sh, txx, q, ctx->num_sms);
       ctx->launches++;
       // the final control also advances the iteration and, inside the WHILE
       // graph, sets the loop condition
-      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_TN2, post(POST_FINAL, h), t2d ? nch_p : 0)))
+      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_TN2, post(POST_FINAL, h), nch_s, st.flag)))
         break;
       cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) e = sch_fail(ctx, SCH_ERR_CUDA, "dd cg launch: %s", cudaGetErrorString(le));

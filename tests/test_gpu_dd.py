@@ -359,3 +359,73 @@ def test_dd_hmc_update_antiperiodic_matches_reference(scheme, G):
         assert abs(s.dh - so["dh"]) < 1e-8
         assert s.accepted == so["accepted"] and s.inversions == so["inversions"]
     assert np.max(np.abs(npy(lat.gather_links(q_ext)) - qo)) < 1e-8
+
+
+_MARCH_SNIPPET = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice
+out = {}
+for L, T, G in [(32, 8, 1), (64, 56, 2), (48, 200, 3), (16, 2048, 2), (256, 96, 4)]:
+    rng = np.random.default_rng(L * T + G)
+    q = rng.uniform(-np.pi, np.pi, (2, L, T))
+    psi = rng.standard_normal((L, T, 2)) + 1j * rng.standard_normal((L, T, 2))
+    lat = StripLattice(L, T, strips=G)
+    op = DDWilsonDirac(lat, lat.scatter_links(q), 0.1)
+    out[f"n_{L}_{T}"] = lat.gather_spinor(op.normal(lat.scatter_spinor(psi))).cpu().numpy()
+    x, it, rel = op.cg(lat.scatter_spinor(psi), 1e-10)
+    out[f"x_{L}_{T}"] = lat.gather_spinor(x).cpu().numpy()
+    out[f"it_{L}_{T}"] = np.array([it])
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_dd_marching_pass_equals_tile_kernels(tmp_path):
+    """The warp-marching stencil pass (csrc/march.cuh, the default) against
+    the shared-memory tile kernels (SCH_DD_MARCH=0) on rows shorter than a
+    warp's band (T = 8), of whole bands (56), with a clipped last band (200,
+    96) and of cfg5's length (2048: 512 row partials per row through the
+    coalesced canonical sum): D^dag D to 1e-13, the same CG iteration counts,
+    solutions to 1e-12.  The switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for m in ("0", "1"):
+        path = tmp_path / f"march{m}.npz"
+        env = dict(os.environ, SCH_DD_MARCH=m)
+        subprocess.run([sys.executable, "-c", _MARCH_SNIPPET, root, str(path)], check=True, env=env,
+                       timeout=600)
+        res[m] = np.load(path)
+    for k in res["0"].files:
+        a, b = res["0"][k], res["1"][k]
+        if k.startswith("it_"):
+            np.testing.assert_array_equal(a, b, err_msg=k)
+        else:
+            assert rel_err(b, a) < (1e-13 if k.startswith("n_") else 1e-12), (k, rel_err(b, a))
+
+
+def test_dd_marching_pass_cfg5_rows_match_oracle():
+    """Rows of cfg5's length on a short lattice (16 x 2048, two strips)
+    against the oracle: D^dag D to 1e-12, CG iteration count and solution."""
+    from paper_1512_03812_b200.dd import DDWilsonDirac, StripLattice
+    from oracle import schwinger_oracle as O
+    L, T = 16, 2048
+    rng = np.random.default_rng(2048)
+    q = rng.uniform(-np.pi, np.pi, (2, L, T))
+    psi = rng.standard_normal((L, T, 2)) + 1j * rng.standard_normal((L, T, 2))
+    U = O.fermion_links(q)
+    runs = []
+    for G in (1, 2):
+        lat = StripLattice(L, T, strips=G)
+        op = DDWilsonDirac(lat, lat.scatter_links(q), 0.1)
+        got = npy(lat.gather_spinor(op.normal(lat.scatter_spinor(psi))))
+        assert rel_err(got, O.normal_op(U, psi, 0.1)) < 1e-12
+        x, it, rel = op.cg(lat.scatter_spinor(psi), 1e-10)
+        runs.append((npy(lat.gather_spinor(x)), it, rel))
+    assert runs[0][1:] == runs[1][1:] and np.array_equal(runs[0][0], runs[1][0])
+    xo, ito, _ = O.cg_normal(U, 0.1, psi, 1e-10)
+    assert runs[0][1] == ito and rel_err(runs[0][0], xo) < 1e-12
