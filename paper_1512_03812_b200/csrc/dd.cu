@@ -146,11 +146,10 @@ struct DDState {
   double* sc;   // scalars: see SC_* below
   int* flag;    // [S] need_x (X pass) per local strip (all equal)
   double* beta; // [S] beta per local strip (all equal)
-  int* ctl;     // [0] done, [1] iters, [2] status, [3] current iteration (device-side loop),
-                // [4] deferred update: which direction buffer holds the current p
+  int* ctl;     // [0] done, [1] iters, [2] status, [3] current iteration (device-side loop)
 };
 enum { SC_NORMB2 = 0, SC_PAP, SC_RR, SC_TN2, SC_RS, SC_RSNEW, SC_ALPHA, SC_NORMB, SC_TARGET,
-       SC_BEST, SC_RELRES, SC_XPEND, SC_COUNT };
+       SC_BEST, SC_RELRES, SC_COUNT };
 
 SCH_DEV bool own_row(long long i, int T, int Lext, int lo, int hi) {
   const int row = (int)((i / T) % Lext);
@@ -164,12 +163,7 @@ SCH_DEV bool own_row(long long i, int T, int Lext, int lo, int hi) {
 SCH_DEV void dd_alpha(DDState st) {
   if (st.ctl[0]) return;
   const double den = st.sc[SC_PAP];
-  const double al = den > 0.0 ? st.sc[SC_RS] / den : 0.0;
-  st.sc[SC_ALPHA] = al;
-  // deferred solution update (marching pass): x += alpha p is now pending, p
-  // being the direction the stencil pass of this iteration just stored
-  st.sc[SC_XPEND] = al;
-  st.ctl[4] = (st.ctl[3] & 1) ^ 1;
+  st.sc[SC_ALPHA] = den > 0.0 ? st.sc[SC_RS] / den : 0.0;
 }
 
 SCH_DEV void dd_check(DDState st, int S) {
@@ -192,7 +186,6 @@ SCH_DEV void dd_final(DDState st, int S, int maxiter) {
   const int nx = st.flag[0];
   double rs_new = st.sc[SC_RSNEW];
   if (nx) {
-    st.sc[SC_XPEND] = 0.0;   // k_dd_xfix applied it ahead of the true-residual pass
     const double tn2 = st.sc[SC_TN2];
     const double tn = sqrt(tn2);
     const int repl = (it % kDDReplace) == 0;
@@ -738,8 +731,6 @@ __global__ void k_dd_ctrl_init(DDState st, int S, double tol, int have_x0) {
   st.sc[SC_RS] = have_x0 ? st.sc[SC_RR] : nb2;
   st.sc[SC_BEST] = INFINITY;
   st.sc[SC_RELRES] = 0.0;
-  st.sc[SC_XPEND] = 0.0;
-  st.ctl[4] = 1;
   for (int s = 0; s < S; ++s) {
     st.beta[s] = 0.0;
     st.flag[s] = 0;
@@ -786,55 +777,6 @@ __global__ void k_dd_update(double2* __restrict__ r, double2* __restrict__ p, do
       if (lane == 0) rowpart[((long long)c.s * (hi - lo) + (c.xr - lo)) * nch + c.ch] = t;
     }
   }
-}
-
-// ---- Deferred solution update (the marching stencil pass, march.cuh MODE_PU)
-// k_dd_update reads r, p, x, ap and writes r, p, x: 224 B/site, on top of
-// the stencil pass's 128.  The stencil pass forms p = r + beta p_old anyway
-// and reads p_old anyway, so it can store p (into the other of two direction
-// buffers) and apply the PREVIOUS iteration's x += alpha p_old while it has
-// p_old in registers: it then moves 224 B/site and what is left for the
-// second pass is r -= alpha ap with ||r||^2 (96 B/site) — 320 instead of
-// 352 B per site and iteration, the same values in the same order
-// (x_{k+1} = fma(alpha_k, p_k, x_k), only later).  When an iteration needs
-// the true residual (stop test passed, or residual replacement) k_dd_xfix
-// brings x up to date first; after the loop it applies a still pending update.
-__global__ void k_dd_update_r(double2* __restrict__ r, const double2* __restrict__ ap, DDState st, int S,
-                              int Lext, int T, int CW, int lo, int hi, double* __restrict__ rowpart) {
-  if (st.ctl[0]) return;
-  if ((st.ctl[3] % kDDReplace) == 0) return;   // the true-residual pass forms r
-  const double al = st.sc[SC_ALPHA];
-  const int lane = threadIdx.x & 31, K = CW > 32 ? 2 : 1, nch = T / CW, own = hi - lo;
-  const long long items = (long long)S * own * nch;
-  const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
-  for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += nw) {
-    const ChunkItem c = chunk_item(w, nch, own);
-    double v[2] = {0.0, 0.0};
-    for (int k = 0; k < K; ++k) {
-      const int j = lane * K + k;
-      if (j >= CW) continue;
-      const long long i = ((long long)c.s * Lext + lo + c.xr) * T + c.ch * CW + j;
-      const Spinor rv = sp_fma(-al, ld256_spinor_nc(ap, i), ld256_spinor(r, i));
-      st256_spinor(r, i, rv);
-      v[k] = spinor_norm2(rv);
-    }
-    const double t = warp_tree_sum(v[0] + v[1]);
-    if (lane == 0) rowpart[((long long)c.s * own + c.xr) * nch + c.ch] = t;
-  }
-}
-
-// x += pending alpha * p on every row.  In the loop (final = 0): only when
-// the stop test asked for the true residual; the control after that pass
-// clears the pending alpha.  After the loop (final = 1): whatever is pending.
-__global__ void k_dd_xfix(double2* __restrict__ x, const double2* __restrict__ p0,
-                          const double2* __restrict__ p1, DDState st, long long nsites, int final) {
-  if (!final && (st.ctl[0] || st.flag[0] == 0)) return;
-  const double al = st.sc[SC_XPEND];
-  if (al == 0.0) return;
-  const double2* p = st.ctl[4] ? p1 : p0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nsites;
-       i += (long long)gridDim.x * blockDim.x)
-    st256_spinor(x, i, sp_fma(al, ld256_spinor_nc(p, i), ld256_spinor(x, i)));
 }
 
 // Row partials of the Hamiltonian's sums over the own rows (site values:
@@ -1109,9 +1051,7 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   const int nch_s = dd_stencil_nch(dd, skind);              // chunks per row of the stencil pass (0: NC)
   const int nch_p = nch_s ? nch_s : dd->NC;
   const size_t npart = (size_t)dd->S * dd->Lloc * std::max(dd->NC, nch_p);   // row partials
-  // the marching pass defers the solution update (k_dd_update_r): a second direction buffer
-  const bool defer = skind == ST_MARCH && march_defer_enabled();
-  const size_t bytes = (defer ? 4 : 3) * vec + sizeof(double) * (2 * npart + SC_COUNT + dd->S + 64) +
+  const size_t bytes = 3 * vec + sizeof(double) * (2 * npart + SC_COUNT + dd->S + 64) +
                        sizeof(int) * (dd->S + 8) + 8 * 256;
   void* ws;
   int rc = sch_workspace(ctx, bytes, &ws);
@@ -1125,7 +1065,6 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   double2* r = (double2*)take(vec);
   double2* p = (double2*)take(vec);
   double2* ap = (double2*)take(vec);
-  double2* p2 = defer ? (double2*)take(vec) : nullptr;
   double* part_a = (double*)take(sizeof(double) * npart);
   double* part_b = (double*)take(sizeof(double) * npart);
   DDState st;
@@ -1174,13 +1113,6 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
   txx.flag = st.flag;
   txx.rowpart = part_b;
 
-  MarchArgs mx{};       // deferred update: p_old = pbuf[iteration & 1] (iteration 1 reads `p`)
-  mx.pbuf[0] = p2;
-  mx.pbuf[1] = p;
-  mx.xq = (double2*)x_ext;
-  mx.xalpha = st.sc + SC_XPEND;
-  mx.ctl = st.ctl;
-
   // One iteration; the iteration number lives on the device (ctl[3]), so the
   // body is the same every time and can be captured.
   auto post = [&](int kind, cudaGraphConditionalHandle h = 0) {
@@ -1199,24 +1131,13 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
     int e = SCH_OK;
     do {
       if ((e = dd_exchange(ctx, dd, (double*)r, 1, 4))) break;
-      if (defer) {
-        launch_dd_march<MODE_PU>(tp, q, ctx->num_sms, &mx);
-        ctx->launches++;
-        if ((e = dd_allsum(ctx, dd, part_a, st.sc + SC_PAP, post(POST_ALPHA), nch_s))) break;
-        k_dd_update_r<<<egrid, 256, 0, q>>>(r, ap, st, dd->S, dd->Lext, dd->T, dd->CW, lo, hi, part_b);
-        ctx->launches++;
-        if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, post(POST_CHECK)))) break;
-        k_dd_xfix<<<egrid, 256, 0, q>>>((double2*)x_ext, p2, p, st, nsites, 0);
-        ctx->launches++;
-      } else {
-        dd_stencil_launch<MODE_P>(skind, sh, tp, q, ctx->num_sms);
-        ctx->launches++;
-        if ((e = dd_allsum(ctx, dd, part_a, st.sc + SC_PAP, post(POST_ALPHA), nch_s))) break;
-        k_dd_update<<<egrid, 256, 0, q>>>(r, p, (double2*)x_ext, ap, st, dd->S, dd->Lext, dd->T, dd->CW,
-                                          lo, hi, part_b);
-        ctx->launches++;
-        if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, post(POST_CHECK)))) break;
-      }
+      dd_stencil_launch<MODE_P>(skind, sh, tp, q, ctx->num_sms);
+      ctx->launches++;
+      if ((e = dd_allsum(ctx, dd, part_a, st.sc + SC_PAP, post(POST_ALPHA), nch_s))) break;
+      k_dd_update<<<egrid, 256, 0, q>>>(r, p, (double2*)x_ext, ap, st, dd->S, dd->Lext, dd->T, dd->CW,
+                                        lo, hi, part_b);
+      ctx->launches++;
+      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, post(POST_CHECK)))) break;
       // x halos are current (x is updated on every row), so no exchange here
       dd_stencil_launch<MODE_X>(skind, sh, txx, q, ctx->num_sms);
       ctx->launches++;
@@ -1277,10 +1198,6 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
       if (*ctx->h_flag) break;
       chunk = std::min(chunk * 2, 32);
     }
-  }
-  if (defer) {   // an update still pending when the loop ended at the iteration cap
-    k_dd_xfix<<<egrid, 256, 0, s>>>((double2*)x_ext, p2, p, st, nsites, 1);
-    SCH_LAUNCHED(ctx);
   }
   int ctl[3];
   double relres;
