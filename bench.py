@@ -1316,9 +1316,14 @@ def run_cfg5(args):
                        "transport": lat.transport},
             "roofline": {"bound": "hbm", "achieved": gbs / max(world, 1), "peak": hbm_peak,
                          "unit": "GB/s per GPU", "frac": gbs / max(world, 1) / hbm_peak,
-                         "peak_kind": peak_kind},
+                         "peak_kind": peak_kind,
+                         "kernel": "k_dd_march<PLAIN, 4-row register ring, 2 CTAs/SM> (warp-marching "
+                                   "fused D^dag D, csrc/march.cuh) + the halo-row copy of each application",
+                         "bytes_model": "96 B/site (psi in + U + out)"},
             "cg": {"iterations": iters, "ms": cg_ms, "ms_per_iteration": cg_ms / max(iters, 1),
-                   "effective_GBs": cg_gbs, "rel_residual": rel},
+                   "effective_GBs": cg_gbs, "effective_frac": cg_gbs / max(world, 1) / hbm_peak,
+                   "bytes_model": "352 B/site/iteration (stencil pass 128 + update pass 224)",
+                   "rel_residual": rel},
             "trajectory": {"scheme": cfg.scheme, "outer": args.outer,
                            "micro_per_call": cfg.micro_per_call, "tau": cfg.tau,
                            "ms": traj_ms, "trajectories_per_s": 1e3 / traj_ms, "dh": traj.dh,

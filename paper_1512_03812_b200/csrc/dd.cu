@@ -52,7 +52,6 @@
 #include "common.cuh"
 #include "runtime.hpp"
 #include "tile.cuh"
-#include "tma2d.cuh"
 #include "march.cuh"
 #include "tma_tile.cuh"
 #include "../../include/schwinger_sm100.h"
@@ -819,28 +818,20 @@ inline unsigned chunk_grid(long long items) {
   return (unsigned)std::max<long long>(1, std::min<long long>((items + 7) / 8, 148 * 8));
 }
 
-// The TMA-pipelined 2-D tile pass (tma2d.cuh) for the D^dag D and the CG's
-// stencil pass (T a multiple of 32); SCH_DD_TMA2D=0 keeps the
-// one-tile-per-CTA halo kernel
-bool dd_use_tma2d(const sch_dd* dd) { return tma2d_enabled() && tma2d_shape_ok(dd->Lloc, dd->T); }
-
 // The stencil pass of the decomposed lattice: the warp-marching register
-// kernel (march.cuh; SCH_DD_MARCH=0 turns it off), else the TMA 2-D tile
-// kernel (T a multiple of 32), else the one-tile-per-CTA halo kernel.  All
-// three write canonical row-chunk partials; only the chunk width differs.
-enum { ST_TILE = 0, ST_TMA2D = 1, ST_MARCH = 2 };
+// kernel (march.cuh), else — SCH_DD_MARCH=0, or rows beyond 8192 sites — the
+// one-tile-per-CTA halo kernel.  Both write canonical row-chunk partials;
+// only the chunk width differs.  (Round 2's TMA 2-D tile kernel, 55 % of HBM
+// on cfg5 against the marching pass's 80-89 %, was removed.)
+enum { ST_TILE = 0, ST_MARCH = 2 };
 int dd_stencil_kind(const sch_dd* dd) {
-  if (march_enabled() && march_shape_ok(dd->T)) return ST_MARCH;
-  return dd_use_tma2d(dd) ? ST_TMA2D : ST_TILE;
+  return march_enabled() && march_shape_ok(dd->T) ? ST_MARCH : ST_TILE;
 }
 // chunks per row of the stencil pass's partials (0: the lattice's own NC)
-int dd_stencil_nch(const sch_dd* dd, int kind) {
-  return kind == ST_MARCH ? march_nch(dd->T) : kind == ST_TMA2D ? dd->T / kT2T : 0;
-}
+int dd_stencil_nch(const sch_dd* dd, int kind) { return kind == ST_MARCH ? march_nch(dd->T) : 0; }
 template <int MODE>
 void dd_stencil_launch(int kind, const TileShape& sh, const TileArgs& a, cudaStream_t st, int num_sms) {
   if (kind == ST_MARCH && launch_dd_march<MODE>(a, st, num_sms)) return;
-  if (kind == ST_TMA2D && launch_dd_tma2d<MODE>(a, st, num_sms)) return;
   launch_dd_tile<MODE>(sh, a, st);
 }
 

@@ -1,9 +1,9 @@
 // Warp-marching fused D^dag D for the decomposed lattice (BASELINE
 // configs[4]: rows of T = 2048 sites; fermion.py:129-131, fermion.py:194).
 //
-// The tile kernels (tile.cuh, tma2d.cuh) stage a 2-D region in shared memory
-// and run D, then D^dag, as barrier-separated phases of a CTA: at 2048^2
-// they reach 49-55 % of HBM, bound by those phases (ncu: barrier and
+// The tile kernels (tile.cuh; round 2's TMA-pipelined 2-D variant) stage a
+// 2-D region in shared memory and run D, then D^dag, as barrier-separated
+// phases of a CTA: at 2048^2 they reach 49-55 % of HBM, bound by those phases (ncu: barrier and
 // short-scoreboard stalls) and not by the memory system.  Here there is no
 // shared memory and no barrier: a WARP owns a band of kMarchW = 28 time
 // columns (lane l holds column c0 - 2 + l, i.e. the band plus the two halo

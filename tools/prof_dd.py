@@ -1,6 +1,6 @@
 """ncu driver: a few iterations of the decomposed CG on cfg5's 2048^2 lattice.
 
-    python tools/prof_dd.py [transport] [strips]
+    python tools/prof_dd.py [transport] [strips] [cg|normal]
 """
 import sys
 from pathlib import Path
@@ -19,7 +19,11 @@ rng = np.random.default_rng(5)
 lat = StripLattice(L, L, strips=strips, transport=transport)
 op = DDWilsonDirac(lat, lat.scatter_links(rng.uniform(-np.pi, np.pi, (2, L, L))), 0.05)
 psi = lat.scatter_spinor(rng.standard_normal((L, L, 2)) + 1j * rng.standard_normal((L, L, 2)))
-for _ in range(2):
+what = sys.argv[3] if len(sys.argv) > 3 else "cg"
+if what == "normal":   # the D^dag D alone (halo exchange + the stencil pass)
+    for _ in range(4):
+        op.normal(psi)
+for _ in range(0 if what == "normal" else 2):
     try:
         op.cg(psi, 1e-10, maxiter=12)
     except SolverError:
