@@ -27,6 +27,14 @@
 
 #include "block_stencil.cuh"
 
+// Phase stamps of the iteration for tools/micro/resblk_phases.cu (which
+// defines them as clock reads by thread 0); nothing in the library build.
+#ifndef RES_STAMP
+#define RES_STAMP(i)
+#define RES_STAMP_BEGIN()
+#define RES_STAMP_END(iters)
+#endif
+
 //
 // TSH = 1 moves the t-direction faces from shared memory to warp shuffles:
 // a block row of NBT = TC/BT threads is contiguous in the thread index, so
@@ -231,13 +239,17 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
 
   double best = INFINITY;
   double inv_rs = __drcp_rn(rs);
+  RES_STAMP_BEGIN();
   for (int it = 1; it <= a.maxiter; ++it) {
+    RES_STAMP(0);
     // w = D^dag D p; <p, D^dag D p> formed as ||D p||^2 during the D stage
     // and published by the barrier between the stages (resident.cuh)
     {
       Spinor t[SPT];
       stage_pre(F{}, E0, p, t);
+      RES_STAMP(1);
       __syncthreads();
+      RES_STAMP(2);
       stage_post(F{}, E0, t);
       double dd = 0.0;
 #pragma unroll
@@ -249,8 +261,11 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
         dd = warp_sum(dd);
         if ((tid & 31) == 0) red[0][tid >> 5] = dd;
       }
+      RES_STAMP(3);
       __syncthreads();
+      RES_STAMP(4);
       stage_post(T{}, E1, w);
+      RES_STAMP(5);
     }
     double den;
     if constexpr (P4) {
@@ -261,6 +276,7 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
       for (int q = 1; q < NW; ++q) den += red[0][q];
     }
     const double alpha = den > 0.0 ? rs / den : 0.0;
+    RES_STAMP(6);
     const bool repl = (it % kResReplace) == 0;
     double nrm[SPT];
 #pragma unroll
@@ -281,8 +297,10 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
     const double rsn = repl ? 0.0 : nrm[0];
     double rs_new = 0.0;
     bool check = true;
+    RES_STAMP(7);
     if (!repl) {
       rs_new = P4 ? part4_block_sum<NW>(rsn, red4[1]) : block_sum<NT>(rsn, red[1]);
+      RES_STAMP(8);
       check = rs_new <= t2lo;
       if (!check && rs_new <= t2hi) {   // inside the band: the exact test (asm keeps
         double sq;                      // the compiler from hoisting the sqrt)
@@ -324,7 +342,9 @@ SCH_DEV void cg_resblk_run(const ResArgs& a, int c, long long cb, double2* sm) {
     for (int k = 0; k < SPT; ++k) p[k] = sp_fma(beta, p[k], r[k]);
     rs = rs_new;
     inv_rs = __drcp_rn(rs);
+    RES_STAMP(9);
   }
+  RES_STAMP_END(a.maxiter);
 #pragma unroll
   for (int k = 0; k < SPT; ++k) st_x(cb + site(k), x[k]);
   if (tid == 0) {
