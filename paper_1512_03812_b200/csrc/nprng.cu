@@ -17,6 +17,8 @@
 // The generator state lives in device memory between calls, so a chain's
 // stream advances exactly as the reference's Generator object would.
 #include "common.cuh"
+#include <cstdlib>
+
 #include "runtime.hpp"
 #include "../_lib/gen/ziggurat_tables.h"
 #include "../../include/schwinger_sm100.h"
@@ -53,6 +55,68 @@ __device__ __forceinline__ void philox_block(uint64_t x0, uint64_t x1, uint64_t 
     kb += kW1;
   }
   o0 = x0; o1 = x1; o2 = x2; o3 = x3;
+}
+
+// log1p(x) for x in (-1, 0] (the ziggurat tail's log1p(-u)), operation by
+// operation what the reference's libm evaluates: glibc's log1p (the fdlibm
+// algorithm with its polynomial split in four, as glibc evaluates it), built
+// with FMA contraction as the variant x86-64 hosts with FMA dispatch to —
+// checked here against the host libm on 2e7 arguments (0 differences; CUDA's
+// log1p differs from it in the last bit for ~0.4 % of arguments) and by the
+// stream tests against NumPy itself.  Every operation is an explicit
+// intrinsic, so nvcc contracts nothing else.
+__device__ double np_log1p_neg(double x) {
+  const double ln2_hi = 6.93147180369123816490e-01, ln2_lo = 1.90821492927058770002e-10;
+  const double Lp1 = 6.666666666666735130e-01, Lp2 = 3.999999999940941908e-01,
+               Lp3 = 2.857142874366239149e-01, Lp4 = 2.222219843214978396e-01,
+               Lp5 = 1.818357216161805012e-01, Lp6 = 1.531383769920937332e-01,
+               Lp7 = 1.479819860511658591e-01;
+  const int hx = __double2hiint(x), ax = hx & 0x7fffffff;
+  if (hx > 0 || ax >= 0x3ff00000) return log1p(x);   // outside (-1, 0]: not the tail's argument
+  int k = 1, hu = 0;
+  double f = 0.0, c = 0.0;
+  if (ax < 0x3e200000) {                               // |x| < 2^-29
+    if (ax < 0x3c900000) return x;                     // |x| < 2^-54
+    return __fma_rn(-0.5, __dmul_rn(x, x), x);
+  }
+  if (hx <= (int)0xbfd2bec3) {                         // -0.2929 < x
+    k = 0;
+    f = x;
+    hu = 1;
+  } else {
+    double u = __dadd_rn(1.0, x);
+    hu = __double2hiint(u);
+    k = (hu >> 20) - 1023;
+    c = k > 0 ? __dsub_rn(1.0, __dsub_rn(u, x)) : __dsub_rn(x, __dsub_rn(u, 1.0));
+    c = __ddiv_rn(c, u);
+    hu &= 0x000fffff;
+    if (hu < 0x6a09e) {
+      u = __hiloint2double(hu | 0x3ff00000, __double2loint(u));
+    } else {
+      k += 1;
+      u = __hiloint2double(hu | 0x3fe00000, __double2loint(u));
+      hu = (0x00100000 - hu) >> 2;
+    }
+    f = __dsub_rn(u, 1.0);
+  }
+  const double hfsq = __dmul_rn(__dmul_rn(0.5, f), f);
+  const double dk = (double)k;
+  if (hu == 0) {                                       // |f| < 2^-20
+    if (f == 0.0) return k == 0 ? 0.0 : __fma_rn(dk, ln2_hi, __fma_rn(dk, ln2_lo, c));
+    const double R = __dmul_rn(__fma_rn(-0.66666666666666666, f, 1.0), hfsq);
+    if (k == 0) return __dsub_rn(f, R);
+    return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(R, __fma_rn(dk, ln2_lo, c)), f));
+  }
+  const double s = __ddiv_rn(f, __dadd_rn(f, 2.0));
+  const double z = __dmul_rn(s, s);
+  const double R4 = __fma_rn(z, Lp7, Lp6), R3 = __fma_rn(z, Lp5, Lp4), R2 = __fma_rn(z, Lp3, Lp2);
+  const double z2 = __dmul_rn(z, z), z4 = __dmul_rn(z2, z2), z6 = __dmul_rn(z2, z4);
+  double R = __fma_rn(z, Lp1, __dmul_rn(z2, R2));
+  R = __fma_rn(z4, R3, R);
+  R = __fma_rn(z6, R4, R);
+  const double t = __dmul_rn(__dadd_rn(R, hfsq), s);
+  if (k == 0) return __dsub_rn(f, __dsub_rn(hfsq, t));
+  return __fma_rn(dk, ln2_hi, -__dsub_rn(__dsub_rn(hfsq, __dadd_rn(t, __fma_rn(dk, ln2_lo, c))), f));
 }
 
 struct Gen {
@@ -105,8 +169,8 @@ struct Gen {
       } else if (idx == 0) {
         bool tail = false;
         while (!tail) {
-          const double xx = -kZigInvR * log1p(-next_double());
-          const double yy = -log1p(-next_double());
+          const double xx = -kZigInvR * np_log1p_neg(-next_double());
+          const double yy = -np_log1p_neg(-next_double());
           if (yy + yy > xx * xx) {
             result = ((rabs >> 8) & 0x1) ? -(kZigR + xx) : kZigR + xx;
             tail = true;
@@ -159,6 +223,14 @@ struct WarpGen {
     a = a0 = s.pos;
     filled = 0;
   }
+  // start at absolute word `start` (the parallel walk's chunks); a0 = -1: the
+  // state is always written back
+  __device__ void load_at(const NpPhilox& s, uint64_t* ring_, int lane_, long long start) {
+    load(s, ring_, lane_);
+    a = start;
+    a0 = -1;
+    filled = (start / 4) * 4;
+  }
   // block j >= 1 after ctr0 (256-bit add)
   __device__ void block_at(long long j, uint64_t& o0, uint64_t& o1, uint64_t& o2, uint64_t& o3) const {
     uint64_t x0 = c0 + (uint64_t)j, x1 = c1, x2 = c2, x3 = c3;
@@ -185,42 +257,78 @@ struct WarpGen {
   }
   __device__ double next_double() { return (double)(next_u64() >> 11) * (1.0 / 9007199254740992.0); }
 
-  // one complete NumPy standard_normal, run redundantly by every lane
-  __device__ double normal_serial() {
-    double result = 0.0;
-    bool done = false;
-    while (!done) {
-      uint64_t r = next_u64();
-      const int idx = (int)(r & 0xff);
-      r >>= 8;
-      const int sign = (int)(r & 0x1);
-      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
-      double x = (double)rabs * np_wi_double[idx];
-      if (sign & 0x1) x = -x;
-      if (rabs < np_ki_double[idx]) {
-        result = x;
-        done = true;
-      } else if (idx == 0) {
-        bool tail = false;
-        while (!tail) {
-          const double xx = -kZigInvR * log1p(-next_double());
-          const double yy = -log1p(-next_double());
-          if (yy + yy > xx * xx) {
-            result = ((rabs >> 8) & 0x1) ? -(kZigR + xx) : kZigR + xx;
-            tail = true;
-          }
-        }
-        done = true;
-      } else {
-        const double u = next_double();
-        if (__dadd_rn(__dmul_rn(np_fi_double[idx - 1] - np_fi_double[idx], u), np_fi_double[idx]) <
-            exp(-0.5 * x * x)) {
-          result = x;
-          done = true;
+  // one pass of NumPy's random_standard_normal loop at word a, run redundantly
+  // by every lane: consumes the words the reference consumes; true if the
+  // pass returned a value
+  __device__ bool attempt_serial(double& result) {
+    uint64_t r = next_u64();
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 0x1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    double x = (double)rabs * np_wi_double[idx];
+    if (sign & 0x1) x = -x;
+    if (rabs < np_ki_double[idx]) {
+      result = x;
+      return true;
+    }
+    if (idx == 0) {
+      for (;;) {
+        const double xx = -kZigInvR * np_log1p_neg(-next_double());
+        const double yy = -np_log1p_neg(-next_double());
+        if (yy + yy > xx * xx) {
+          result = ((rabs >> 8) & 0x1) ? -(kZigR + xx) : kZigR + xx;
+          return true;
         }
       }
     }
+    // two roundings, as NumPy's baseline-x86 build evaluates it (no FMA)
+    const double u = next_double();
+    if (__dadd_rn(__dmul_rn(np_fi_double[idx - 1] - np_fi_double[idx], u), np_fi_double[idx]) <
+        exp(-0.5 * x * x)) {
+      result = x;
+      return true;
+    }
+    return false;
+  }
+  // one complete NumPy standard_normal
+  __device__ double normal_serial() {
+    double result = 0.0;
+    while (!attempt_serial(result)) {
+    }
     return result;
+  }
+
+  // The passes that START at words [a, end): emit(g, value) for the values
+  // they return, numbered g0, g0 + 1, ... and stopping at N.  Returns the
+  // number emitted; `a` is left behind the last pass's words (it may lie
+  // beyond `end`: a pass that starts inside the chunk runs to its end).
+  template <class Emit>
+  __device__ long long walk(long long end, long long g0, long long N, Emit emit) {
+    long long g = g0;
+    while (a < end && g < N) {
+      ensure(a + 31);
+      uint64_t r = ring[(a + lane) % kRing];
+      const int idx = (int)(r & 0xff);
+      r >>= 8;
+      const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+      double x = (double)rabs * np_wi_double[idx];
+      if (r & 0x1) x = -x;
+      const unsigned slow = __ballot_sync(0xffffffffu, a + lane < end && !(rabs < np_ki_double[idx]));
+      const int f = slow ? __ffs(slow) - 1 : 32;
+      const long long k = min(min((long long)f, end - a), N - g);
+      if (lane < k) emit(g + lane, x);
+      a += k;
+      g += k;
+      if (k == f && a < end && g < N) {   // word a starts a slow pass
+        double y;
+        if (attempt_serial(y)) {
+          if (lane == 0) emit(g, y);
+          ++g;
+        }
+      }
+    }
+    return g - g0;
   }
 
   // n normals, out[i * stride] = scale * N_i (scale 1 leaves the value exact)
@@ -274,7 +382,224 @@ struct WarpGen {
   }
 };
 
+// ---------------------------------------------------------------------------
+// One long stream walked by the whole GPU (the decomposed lattice's heatbath
+// draws 6 * L * T normals from ONE reference stream: a single warp needs
+// 0.5 s for cfg5's 25 M).  The words of a stream are random-access (Philox is
+// counter based); only the ziggurat's passes are serial, because a pass that
+// leaves the fast path consumes extra words.  The stream's words are cut into
+// chunks of kChunk:
+//   A  every warp walks its chunk as if a pass started at the chunk's first
+//      word: how many values the passes starting in the chunk return (cnt)
+//      and how many words the last one runs past the chunk's end (over);
+//   B  one warp goes through the chunks in order: the entry offset of chunk
+//      k is the overrun of chunk k-1, and the numbering of its first value
+//      the running sum of the counts.  Where the entry offset is not 0 (1 %
+//      of the chunks) the chunk's count is corrected by walking both entry
+//      points until they meet (two neighbouring passes meet at once unless
+//      one is a slow pass: a few words);
+//   C  every warp walks its chunk again from its true entry and writes the
+//      values to their places; the warp that writes value N-1 stores the
+//      generator state (NumPy's: block of the last consumed word, position);
+//   D  if the chunks did not hold N values (they are sized for 1.02 words per
+//      value; 1.0127 expected), one warp continues serially.
+// Values and final state are those of the serial walk, bit for bit.
+constexpr int kChunk = 2048;
+
+struct OutMap {   // where value g of the stream goes
+  double *p, *phi;
+  long long V2;   // heatbath: 2 V values to p, then 2 V to Re phi, 2 V to Im phi (both x s)
+  double s;
+  int heatbath;
+  __device__ void put(long long g, double x) const {
+    if (!heatbath || g < V2) p[g] = x;
+    else if (g < 2 * V2) phi[2 * (g - V2)] = x * s;
+    else phi[2 * (g - 2 * V2) + 1] = x * s;
+  }
+};
+
+struct ParArgs {
+  NpPhilox* st;
+  long long N;
+  int K;
+  int *cnt, *over, *entry;
+  long long* pref;
+  long long* tot;   // [0] values the chunks hold (capped at N), [1] first word after the chunks' passes
+  NpPhilox* st_end; // the state after value N-1, written by the warp that emits it (the other
+                    // warps of that launch still read *st); the last kernel moves it to *st
+  OutMap om;
+};
+
+// scalar random access to the stream's words (phase B's corrections)
+struct WordAt {
+  uint64_t c0, c1, c2, c3, k0, k1, b[4];
+  long long cached;
+  uint64_t w[4];
+  __device__ void load(const NpPhilox& s) {
+    c0 = s.ctr[0]; c1 = s.ctr[1]; c2 = s.ctr[2]; c3 = s.ctr[3];
+    k0 = s.key[0]; k1 = s.key[1];
+    for (int e = 0; e < 4; ++e) b[e] = s.buf[e];
+    cached = -1;
+  }
+  __device__ uint64_t at(long long i) {
+    const long long j = i / 4;
+    if (j != cached) {
+      if (j == 0) {
+        for (int e = 0; e < 4; ++e) w[e] = b[e];
+      } else {
+        uint64_t x0 = c0 + (uint64_t)j, x1 = c1, x2 = c2, x3 = c3;
+        if (x0 < c0 && ++x1 == 0 && ++x2 == 0) ++x3;
+        philox_block(x0, x1, x2, x3, k0, k1, w[0], w[1], w[2], w[3]);
+      }
+      cached = j;
+    }
+    return w[i % 4];
+  }
+  __device__ double dbl(long long i) { return (double)(at(i) >> 11) * (1.0 / 9007199254740992.0); }
+  // the pass starting at word i: words consumed, and whether it returns a value
+  __device__ int pass(long long i, bool& value) {
+    uint64_t r = at(i);
+    const int idx = (int)(r & 0xff);
+    r >>= 8;
+    const int sign = (int)(r & 0x1);
+    const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+    value = true;
+    if (rabs < np_ki_double[idx]) return 1;
+    if (idx == 0) {
+      int n = 1;
+      for (;;) {
+        const double xx = -kZigInvR * np_log1p_neg(-dbl(i + n));
+        const double yy = -np_log1p_neg(-dbl(i + n + 1));
+        n += 2;
+        if (yy + yy > xx * xx) return n;
+      }
+    }
+    double x = (double)rabs * np_wi_double[idx];
+    if (sign & 0x1) x = -x;
+    value = __dadd_rn(__dmul_rn(np_fi_double[idx - 1] - np_fi_double[idx], dbl(i + 1)), np_fi_double[idx]) <
+            exp(-0.5 * x * x);
+    return 2;
+  }
+};
+
 constexpr int kWarpsPerBlock = 4;
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) k_np_par_count(ParArgs a) {
+  __shared__ uint64_t rings[kWarpsPerBlock][kRing];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = blockIdx.x * kWarpsPerBlock + w;
+  if (k >= a.K) return;
+  const long long start = a.st->pos + (long long)k * kChunk, end = start + kChunk;
+  WarpGen g;
+  g.load_at(*a.st, rings[w], lane, start);
+  const long long n = g.walk(end, 0, 0x7fffffffffffffffLL, [](long long, double) {});
+  if (lane == 0) {
+    a.cnt[k] = (int)n;
+    a.over[k] = (int)(g.a - end);
+  }
+}
+
+__global__ void __launch_bounds__(32) k_np_par_scan(ParArgs a) {
+  const int lane = threadIdx.x;
+  WordAt wa;
+  wa.load(*a.st);
+  const long long a0 = a.st->pos;
+  int e = 0;            // entry offset of the current chunk (warp-uniform)
+  long long run = 0;    // values before the current chunk
+  for (int k0 = 0; k0 < a.K; k0 += 32) {
+    const int kk = k0 + lane;
+    int n = kk < a.K ? a.cnt[kk] : 0, o = kk < a.K ? a.over[kk] : 0;
+    int my_e = 0;
+    long long my_pref = 0;
+    for (int j = 0; j < 32 && k0 + j < a.K; ++j) {   // every lane runs the same sequence
+      int nj = __shfl_sync(0xffffffffu, n, j), oj = __shfl_sync(0xffffffffu, o, j);
+      if (e != 0) {
+        // passes from the assumed entry (word 0 of the chunk) and from the true
+        // one (word e) until they stand on the same word
+        const long long s0 = a0 + (long long)(k0 + j) * kChunk, end = s0 + kChunk;
+        long long pm = s0, pa = s0 + e;
+        int cm = 0, ca = 0;
+        while (pm != pa && (pm < end || pa < end)) {
+          bool v;
+          if (pm < pa) {
+            const int c = wa.pass(pm, v);
+            if (pm < end) cm += v;
+            pm += c;
+          } else {
+            const int c = wa.pass(pa, v);
+            if (pa < end) ca += v;
+            pa += c;
+          }
+        }
+        if (pm == pa && pm < end) {
+          nj = nj - cm + ca;   // the same passes from the meeting word on
+        } else {               // no common word inside the chunk: the true walk alone
+          while (pa < end) {
+            bool v;
+            const int c = wa.pass(pa, v);
+            ca += v;
+            pa += c;
+          }
+          nj = ca;
+          oj = (int)(pa - end);
+        }
+      }
+      if (lane == j) {
+        my_e = e;
+        my_pref = run;
+      }
+      run += nj;
+      e = oj;
+    }
+    if (kk < a.K) {
+      a.entry[kk] = my_e;
+      a.pref[kk] = my_pref;
+    }
+  }
+  if (lane == 0) {
+    a.tot[0] = run < a.N ? run : a.N;
+    a.tot[1] = a0 + (long long)a.K * kChunk + e;
+  }
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerBlock) k_np_par_emit(ParArgs a) {
+  __shared__ uint64_t rings[kWarpsPerBlock][kRing];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = blockIdx.x * kWarpsPerBlock + w;
+  if (k >= a.K) return;
+  const long long g0 = a.pref[k];
+  if (g0 >= a.N) return;   // warp-uniform
+  const long long start = a.st->pos + (long long)k * kChunk, end = start + kChunk;
+  WarpGen g;
+  g.load_at(*a.st, rings[w], lane, start + a.entry[k]);
+  const OutMap om = a.om;
+  const long long n = g.walk(end, g0, a.N, [&](long long i, double x) { om.put(i, x); });
+  __syncwarp();
+  if (g0 + n == a.N) {   // this warp wrote the last value
+    if (lane == 0) {
+      a.st_end->key[0] = a.st->key[0];
+      a.st_end->key[1] = a.st->key[1];
+      a.st_end->pad = 0;
+    }
+    g.store(*a.st_end);
+  }
+}
+
+// the chunks held fewer than N values: the rest serially, from where they ended
+__global__ void __launch_bounds__(32) k_np_par_rest(ParArgs a) {
+  __shared__ uint64_t ring[kRing];
+  const long long have = a.tot[0];
+  if (have >= a.N) {
+    if (threadIdx.x == 0) *a.st = *a.st_end;
+    return;
+  }
+  WarpGen g;
+  g.load_at(*a.st, ring, threadIdx.x, a.tot[1]);
+  const OutMap om = a.om;
+  g.walk(0x7fffffffffffffffLL, have, a.N, [&](long long i, double x) { om.put(i, x); });
+  __syncwarp();
+  g.store(*a.st);
+}
 
 __global__ void __launch_bounds__(32 * kWarpsPerBlock) k_np_heatbath_w(
     NpPhilox* st, double* __restrict__ p, double* __restrict__ phi, int B, long long V, double s,
@@ -342,6 +667,45 @@ __global__ void k_np_metropolis(NpPhilox* st, const double* __restrict__ dh, int
   g.store(st[c]);
 }
 
+// A few long streams: the parallel walk, stream by stream (the state of
+// stream c is rewritten by its own last kernel only)
+// (SCH_NP_PAR=0 keeps the warp-per-stream walk: the tests compare the two)
+bool par_stream(int B, long long n) {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("SCH_NP_PAR");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on && B <= 8 && n >= (1LL << 17);
+}
+int par_normals(sch_ctx* ctx, NpPhilox* st, long long N, const OutMap& om) {
+  ParArgs a;
+  a.st = st;
+  a.N = N;
+  const long long words = N + N / 50 + 4 * kChunk;   // 1.02 words per value (1.0127 expected)
+  a.K = (int)((words + kChunk - 1) / kChunk);
+  void* ws;
+  const size_t ints = ((size_t)a.K * sizeof(int) + 255) & ~size_t(255);
+  const size_t lls = ((size_t)a.K * sizeof(long long) + 255) & ~size_t(255);
+  int rc = sch_workspace(ctx, 3 * ints + lls + 512, &ws);
+  if (rc) return rc;
+  char* w = (char*)ws;
+  a.cnt = (int*)w;
+  a.over = (int*)(w + ints);
+  a.entry = (int*)(w + 2 * ints);
+  a.pref = (long long*)(w + 3 * ints);
+  a.tot = (long long*)(w + 3 * ints + lls);
+  a.st_end = (NpPhilox*)(w + 3 * ints + lls + 256);
+  a.om = om;
+  const unsigned grid = (unsigned)((a.K + kWarpsPerBlock - 1) / kWarpsPerBlock);
+  k_np_par_count<<<grid, 32 * kWarpsPerBlock, 0, ctx->stream>>>(a);
+  k_np_par_scan<<<1, 32, 0, ctx->stream>>>(a);
+  k_np_par_emit<<<grid, 32 * kWarpsPerBlock, 0, ctx->stream>>>(a);
+  k_np_par_rest<<<1, 32, 0, ctx->stream>>>(a);
+  ctx->launches += 4;
+  return SCH_OK;
+}
+
 unsigned chain_blocks(int B) { return (unsigned)((B + 63) / 64); }
 unsigned warp_blocks(int B) { return (unsigned)((B + kWarpsPerBlock - 1) / kWarpsPerBlock); }
 
@@ -362,6 +726,14 @@ int sch_np_rng_fill(sch_ctx* ctx, void* state, double* out, int B, long long n_p
                     double lo, double hi) {
   SCH_CHECK_ARG(ctx, state && out && B >= 1 && n_per_chain >= 0 && mode >= 0 && mode <= 2,
                 "np_rng_fill: bad args");
+  if (mode == 0 && par_stream(B, n_per_chain)) {
+    for (int c = 0; c < B; ++c) {
+      OutMap om{out + (long long)c * n_per_chain, nullptr, 0, 1.0, 0};
+      const int rc = par_normals(ctx, (NpPhilox*)state + c, n_per_chain, om);
+      if (rc) return rc;
+    }
+    return SCH_OK;
+  }
   k_np_fill_w<<<warp_blocks(B), 32 * kWarpsPerBlock, 0, ctx->stream>>>((NpPhilox*)state, out, B,
                                                                         n_per_chain, mode, lo, hi);
   SCH_LAUNCHED(ctx);
@@ -371,6 +743,15 @@ int sch_np_rng_fill(sch_ctx* ctx, void* state, double* out, int B, long long n_p
 int sch_np_heatbath(sch_ctx* ctx, void* state, double* p, double* phi, int B, long long V,
                     double phi_scale, int quenched) {
   SCH_CHECK_ARG(ctx, state && p && (phi || quenched) && B >= 1 && V >= 1, "np_heatbath: bad args");
+  if (par_stream(B, 2 * V)) {
+    for (int c = 0; c < B; ++c) {
+      OutMap om{p + (long long)c * 2 * V, quenched ? nullptr : phi + (long long)c * 4 * V, 2 * V, phi_scale,
+                quenched ? 0 : 1};
+      const int rc = par_normals(ctx, (NpPhilox*)state + c, quenched ? 2 * V : 6 * V, om);
+      if (rc) return rc;
+    }
+    return SCH_OK;
+  }
   k_np_heatbath_w<<<warp_blocks(B), 32 * kWarpsPerBlock, 0, ctx->stream>>>((NpPhilox*)state, p, phi,
                                                                             B, V, phi_scale, quenched);
   SCH_LAUNCHED(ctx);

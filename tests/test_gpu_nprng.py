@@ -163,3 +163,79 @@ def test_ensemble_checkpoint_resume_and_hand_back_to_reference(tmp_path):
         qo, so = O.ensemble_update(qo, ocfg, rngs)
         assert np.max(np.abs(dha[k] - np.array([s["dh"] for s in so]))) < 1e-8
     assert np.max(np.abs(qa.cpu().numpy() - qo)) < 1e-8
+
+
+def test_long_stream_parallel_walk_is_bit_identical():
+    """A few long streams are walked by the whole GPU (csrc/nprng.cu: chunks
+    of 2048 words counted, scanned with the ~1 % of entry-offset corrections,
+    then emitted): 3 M normals of one stream — wedges, tails, passes that run
+    across chunk ends — are NumPy's bit for bit, from a state that starts in
+    the middle of a Philox block, and the stream continues on the serial path."""
+    import paper_1512_03812_b200 as sw
+    g = sw.NumpyDeviceRng(seed=99, n_chains=1, stream0=4)
+    r = sw.make_rng(99, 4)
+    assert np.array_equal(g.uniform(0.0, 1.0, (3,)).cpu().numpy()[0], r.uniform(0.0, 1.0, size=3))
+    n = 3_000_000
+    got = g.standard_normal((n,)).cpu().numpy()[0]
+    assert np.array_equal(got, r.standard_normal(n))
+    assert np.array_equal(g.standard_normal((11,)).cpu().numpy()[0], r.standard_normal(11))
+    assert g.random().cpu().numpy()[0] == r.random()
+    # a length just above the threshold of the parallel path, twice in a row
+    for m in (131_072, 140_001):
+        assert np.array_equal(g.standard_normal((m,)).cpu().numpy()[0], r.standard_normal(m)), m
+
+
+@pytest.mark.parametrize("quenched", [False, True])
+def test_long_stream_heatbath_matches_reference_order(quenched):
+    """The decomposed lattice's heatbath: p, Re phi, Im phi of a 256 x 256
+    lattice from one stream through the parallel walk (393 k normals), then
+    the Metropolis uniform from the state it leaves."""
+    import paper_1512_03812_b200 as sw
+    from paper_1512_03812_b200.fermion import draw_phi
+    L = 256
+    geom = sw.LatticeGeom(L, L)
+    g = sw.NumpyDeviceRng(seed=5, n_chains=2, stream0=0)
+    p, phi = g.heatbath(geom, quenched=quenched)
+    u = g.random().cpu().numpy()
+    for c in range(2):
+        r = sw.make_rng(5, c)
+        assert np.array_equal(p[c].cpu().numpy(), r.standard_normal((2, L, L)))
+        if not quenched:
+            assert np.array_equal(phi[c].cpu().numpy(), draw_phi(r, L, L))
+        assert u[c] == r.random()
+
+
+_PAR_SNIPPET = r"""
+import sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1512_03812_b200 as sw
+g = sw.NumpyDeviceRng(seed=31, n_chains=3, stream0=9)
+out = {"u": g.uniform(0.0, 1.0, (2,)).cpu().numpy(),
+       "a": g.standard_normal((700_001,)).cpu().numpy(),
+       "b": g.standard_normal((150_000,)).cpu().numpy()}
+p, phi = g.heatbath(sw.LatticeGeom(192, 384))
+out["p"], out["phi"] = p.cpu().numpy(), phi.cpu().numpy()
+out["tail"] = g.standard_normal((5,)).cpu().numpy()
+out["state"] = np.frombuffer(g.state.cpu().numpy().tobytes(), dtype=np.uint8)
+np.savez(sys.argv[2], **out)
+"""
+
+
+def test_long_stream_parallel_walk_equals_serial_walk(tmp_path):
+    """The whole-GPU walk of a long stream against the warp-per-stream walk
+    (SCH_NP_PAR=0) on the same draws: values and the generator state left
+    behind, byte for byte.  The switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    res = {}
+    for m in ("0", "1"):
+        path = tmp_path / f"par{m}.npz"
+        subprocess.run([sys.executable, "-c", _PAR_SNIPPET, root, str(path)], check=True,
+                       env=dict(os.environ, SCH_NP_PAR=m), timeout=600)
+        res[m] = np.load(path)
+    for k in res["0"].files:
+        assert np.array_equal(res["0"][k], res["1"][k]), k
