@@ -242,7 +242,6 @@ __global__ void k_dd_post(DDPost p) { dd_post_run(p); }
 // every strip from its periodic neighbours (local transport).
 __global__ void k_dd_exchange_local(double* __restrict__ f, int S, int P, int Lext, int Lloc, int T,
                                     int W) {
-  pdl_enter();
   const long long row = (long long)T * W;
   const long long n = (long long)S * P * 4 * row;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -272,17 +271,13 @@ __global__ void k_dd_exchange_local(double* __restrict__ f, int S, int P, int Le
 
 int p2p_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W);
 
-// pdl: launch with programmatic stream serialization (the CG iteration's
-// kernels all start with pdl_enter(): each one's launch overlaps its
-// predecessor's tail; SCH_NO_PDL=1 turns it off)
-int dd_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W, bool pdl = false) {
+int dd_exchange(sch_ctx* ctx, sch_dd* dd, double* f, int P, int W) {
   if (dd->p2p) return p2p_exchange(ctx, dd, f, P, W);
   if (dd->comm == nullptr) {
     if (dd->nranks > 1) return sch_fail(ctx, SCH_ERR_ARG, "dd: no transport (NCCL id or p2p connect)");
     const long long n = (long long)dd->S * P * 4 * dd->T * W;
     unsigned grid = (unsigned)std::min<long long>((n + 255) / 256, 148 * 16);
-    launch_k(pdl, k_dd_exchange_local, dim3(grid), dim3(256), 0, ctx->stream, f, dd->S, P, dd->Lext,
-             dd->Lloc, dd->T, W);
+    k_dd_exchange_local<<<grid, 256, 0, ctx->stream>>>(f, dd->S, P, dd->Lext, dd->Lloc, dd->T, W);
     SCH_LAUNCHED(ctx);
     return SCH_OK;
   }
@@ -576,7 +571,6 @@ __global__ void __launch_bounds__(256) k_dd_rowred(RowRed a) {
   __shared__ int last;
   const int b = blockIdx.x, s = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  pdl_enter();
   // The true-residual sum of an iteration whose stop test did not ask for it
   // (its pass wrote nothing, dd_final ignores the value; `need` is the same
   // on every rank, and is rewritten only by the post of this kernel's last
@@ -646,7 +640,7 @@ __global__ void k_dd_tree_post(const double* __restrict__ vals, int G, double* _
 // the global sum of the row partials `part` ([S][Lloc][NC]) into *out (on
 // the device, every rank); `post` runs on the sum
 int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, double* out,
-              const DDPost& post = DDPost{}, int nch = 0, const int* need = nullptr, bool pdl = false) {
+              const DDPost& post = DDPost{}, int nch = 0, const int* need = nullptr) {
   if (!dd->p2p && dd->comm == nullptr && dd->nranks > 1)
     return sch_fail(ctx, SCH_ERR_ARG, "dd: no transport (NCCL id or p2p connect)");
   RowRed a;
@@ -662,7 +656,7 @@ int dd_allsum(sch_ctx* ctx, sch_dd* dd, const double* part, double* out,
   a.out = a.mode == RED_NCCL ? dd->red_all : out;
   a.post = a.mode == RED_LOCAL ? post : DDPost{};
   a.pa = dd->p2p ? p2p_args(dd) : P2PArgs{};
-  launch_k(pdl, k_dd_rowred, dim3(a.nb, dd->S), dim3(256), 0, ctx->stream, a);
+  k_dd_rowred<<<dim3(a.nb, dd->S), 256, 0, ctx->stream>>>(a);
   SCH_LAUNCHED(ctx);
   if (a.mode == RED_P2P) {
     k_p2p_red_finish<<<1, 32, 0, ctx->stream>>>(a.pa, out, post);
@@ -752,7 +746,6 @@ __global__ void k_dd_ctrl_init(DDState st, int S, double tol, int have_x0) {
 __global__ void k_dd_update(double2* __restrict__ r, double2* __restrict__ p, double2* __restrict__ x,
                             const double2* __restrict__ ap, DDState st, int S, int Lext, int T, int CW,
                             int lo, int hi, double* __restrict__ rowpart) {
-  pdl_enter();
   if (st.ctl[0]) return;
   const int repl = (st.ctl[3] % kDDReplace) == 0;
   const double al = st.sc[SC_ALPHA], be = st.beta[0];
@@ -837,9 +830,8 @@ int dd_stencil_kind(const sch_dd* dd) {
 // chunks per row of the stencil pass's partials (0: the lattice's own NC)
 int dd_stencil_nch(const sch_dd* dd, int kind) { return kind == ST_MARCH ? march_nch(dd->T) : 0; }
 template <int MODE>
-void dd_stencil_launch(int kind, const TileShape& sh, const TileArgs& a, cudaStream_t st, int num_sms,
-                       bool pdl = false) {
-  if (kind == ST_MARCH && launch_dd_march<MODE>(a, st, num_sms, pdl)) return;
+void dd_stencil_launch(int kind, const TileShape& sh, const TileArgs& a, cudaStream_t st, int num_sms) {
+  if (kind == ST_MARCH && launch_dd_march<MODE>(a, st, num_sms)) return;
   launch_dd_tile<MODE>(sh, a, st);
 }
 
@@ -1124,28 +1116,25 @@ int sch_dd_cg_normal(sch_ctx* ctx, sch_dd* dd, const double* U_ext, double* b_ex
     p.h = h;
     return p;
   };
-  // programmatic launches between the iteration's kernels: the marching pass
-  // and the local / p2p transports (NCCL's kernels sit between ours there)
-  const bool pdl = use_pdl() && skind == ST_MARCH && dd->comm == nullptr;
   auto iteration = [&](cudaStream_t q, cudaGraphConditionalHandle h) -> int {
     const cudaStream_t saved = ctx->stream;
     ctx->stream = q;   // dd_exchange / dd_allsum enqueue on ctx->stream
     int e = SCH_OK;
     do {
-      if ((e = dd_exchange(ctx, dd, (double*)r, 1, 4, pdl))) break;
-      dd_stencil_launch<MODE_P>(skind, sh, tp, q, ctx->num_sms, pdl);
+      if ((e = dd_exchange(ctx, dd, (double*)r, 1, 4))) break;
+      dd_stencil_launch<MODE_P>(skind, sh, tp, q, ctx->num_sms);
       ctx->launches++;
-      if ((e = dd_allsum(ctx, dd, part_a, st.sc + SC_PAP, post(POST_ALPHA), nch_s, nullptr, pdl))) break;
-      launch_k(pdl, k_dd_update, dim3(egrid), dim3(256), 0, q, r, p, (double2*)x_ext, (const double2*)ap, st,
-               dd->S, dd->Lext, dd->T, dd->CW, lo, hi, part_b);
+      if ((e = dd_allsum(ctx, dd, part_a, st.sc + SC_PAP, post(POST_ALPHA), nch_s))) break;
+      k_dd_update<<<egrid, 256, 0, q>>>(r, p, (double2*)x_ext, ap, st, dd->S, dd->Lext, dd->T, dd->CW,
+                                        lo, hi, part_b);
       ctx->launches++;
-      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, post(POST_CHECK), 0, nullptr, pdl))) break;
+      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_RR, post(POST_CHECK)))) break;
       // x halos are current (x is updated on every row), so no exchange here
-      dd_stencil_launch<MODE_X>(skind, sh, txx, q, ctx->num_sms, pdl);
+      dd_stencil_launch<MODE_X>(skind, sh, txx, q, ctx->num_sms);
       ctx->launches++;
       // the final control also advances the iteration and, inside the WHILE
       // graph, sets the loop condition
-      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_TN2, post(POST_FINAL, h), nch_s, st.flag, pdl)))
+      if ((e = dd_allsum(ctx, dd, part_b, st.sc + SC_TN2, post(POST_FINAL, h), nch_s, st.flag)))
         break;
       cudaError_t le = cudaGetLastError();
       if (le != cudaSuccess) e = sch_fail(ctx, SCH_ERR_CUDA, "dd cg launch: %s", cudaGetErrorString(le));

@@ -86,7 +86,6 @@ SCH_DEV Spinor march_consume(const Spinor& v, double2 hf0, double2 hb0, double2 
 template <int MODE, int PF, int MINB>
 __global__ void __launch_bounds__(32 * kMarchWarps, MINB) k_dd_march(const MarchArgs a) {
   const TileArgs& t = a.t;
-  pdl_enter();
   // the true-residual pass has work only when the stop test asked for it
   if (MODE == MODE_X && t.flag != nullptr && t.flag[0] == 0) return;
   const int lane = threadIdx.x & 31;
@@ -214,7 +213,7 @@ inline int march_nch(int T) { return T / kMarchCW; }
 // PF 1-6 x 2-4 CTAs/SM for all three modes; deeper rings spill, more warps
 // with shallower rings keep fewer bytes in flight.
 template <int MODE, int PF = 4, int MINB = 2>
-inline bool launch_dd_march(const TileArgs& t, cudaStream_t st, int num_sms, bool pdl = false) {
+inline bool launch_dd_march(const TileArgs& t, cudaStream_t st, int num_sms) {
   MarchArgs a;
   a.t = t;
   a.nbt = (t.T + kMarchW - 1) / kMarchW;
@@ -233,6 +232,6 @@ inline bool launch_dd_march(const TileArgs& t, cudaStream_t st, int num_sms, boo
   a.nbx = (nown + a.R - 1) / a.R;
   const long long warps = (long long)t.B * a.nbt * a.nbx;
   const unsigned grid = (unsigned)((warps + kMarchWarps - 1) / kMarchWarps);
-  launch_k(pdl, k_dd_march<MODE, PF, MINB>, dim3(grid), dim3(32 * kMarchWarps), 0, st, a);
+  k_dd_march<MODE, PF, MINB><<<grid, 32 * kMarchWarps, 0, st>>>(a);
   return true;
 }
