@@ -1,4 +1,5 @@
 #!/bin/bash
+# Record of a round-2 experiment (the TMA-ring variant it selects was removed afterwards: no gain).
 # Round-2: marching pass with a per-warp TMA ring (cp.async.bulk + one mbarrier per slot) vs the register ring
 set -u
 O=gpurun_out/exp_r02w
