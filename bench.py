@@ -52,20 +52,20 @@ FALLBACK_HBM = 6650.0
 # The dominant kernel of each ensemble workload, and the DRAM bytes per
 # lattice site of one of its launches measured by ncu --set full (U and b
 # in, x out — the solve itself stays on chip):
-#   cfg3: profiles/r01/ncu_full_k_cg_resblk_tsh.txt, 134.307328 MB read +
-#         36.36352 MB written for 8192 chains x 256 sites (x leaves partly
-#         through L2 after the kernel ends); FP64 pipe 70.1 % active
-#   cfg4: profiles/r01/ncu_full_k_cg_cluster.txt, 268.8832 MB read +
-#         103.359744 MB written for 1024 chains x 4096 sites (b is re-read by
-#         the true-residual checks; part of it misses L2)
-DRAM_CFG4 = (268.8832e6 + 103.359744e6) / (1024 * 4096)
+#   cfg3: profiles/r02/ncu_full_k_cg_resblk_r02.txt, 134.322688 MB read +
+#         36.037888 MB written for 8192 chains x 256 sites (x leaves partly
+#         through L2 after the kernel ends); FP64 pipe 65.5 % active
+#   cfg4: profiles/r02/ncu_cluster_tx.txt, 269.755648 MB read + 103.136512 MB
+#         written for 1024 chains x 4096 sites (b is re-read by the
+#         true-residual checks; part of it misses L2); FP64 pipe 37.4 % active
+DRAM_CFG4 = (269.755648e6 + 103.136512e6) / (1024 * 4096)   # profiles/r02/ncu_cluster_tx.txt
 CG_KERNELS = {
     "cfg3": dict(kernel="k_cg_resblk<16,16,2x2 sites/thread,t-faces by warp shuffle,"
                         "sigma1-diagonal spin basis> (per-chain CG, one 64-thread CTA per chain, "
                         "4 CTAs/SM)",
-                 dram_per_site=(134.252288e6 + 35.547392e6) / (8192 * 256),
-                 fp64_pipe_active=0.652,
-                 source="profiles/r01/ncu_full_k_cg_resblk_rot.txt"),
+                 dram_per_site=(134.322688e6 + 36.037888e6) / (8192 * 256),
+                 fp64_pipe_active=0.655,
+                 source="profiles/r02/ncu_full_k_cg_resblk_r02.txt"),
     "cfg3_mega": dict(kernel="k_traj_anfg16 (trajectory megakernel: one 64-thread CTA per 16x16 "
                              "chain runs H(start), the 17 resident-CG solves, forces, FG terms, "
                              "inner leapfrogs and H(end) of the adapted-nested-fg trajectory)",
@@ -75,8 +75,8 @@ CG_KERNELS = {
                         "4-CTA cluster per chain, faces and partial sums pushed with st.async "
                         "onto the receiver's mbarrier)",
                  dram_per_site=DRAM_CFG4,
-                 fp64_pipe_active=0.431,
-                 source="profiles/r01/ncu_full_k_cg_cluster.txt"),
+                 fp64_pipe_active=0.374,
+                 source="profiles/r02/ncu_cluster_tx.txt"),
 }
 
 CFG3 = dict(L=16, T=16, beta=2.0, m0=0.1, tau=1.0, scheme="adapted-nested-fg", micro_per_call=2,
