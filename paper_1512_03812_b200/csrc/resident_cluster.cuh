@@ -25,6 +25,14 @@
 #include "block_stencil.cuh"
 #include "tma_tile.cuh"
 
+// Phase stamps of the iteration for tools/micro/cluster_phases.cu (clock
+// reads by thread 0 of the cluster's first CTA); nothing in the library build.
+#ifndef RES_STAMP
+#define RES_STAMP(i)
+#define RES_STAMP_BEGIN()
+#define RES_STAMP_END(iters)
+#endif
+
 SCH_DEV void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory"); }
 SCH_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory"); }
 SCH_DEV void cluster_barrier() {
@@ -261,24 +269,33 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
   int it = 1;
   int status = 1;
   double relres = 0.0;
+  RES_STAMP_BEGIN();
   for (; it <= a.maxiter; ++it) {
+    RES_STAMP(0);
     double dd;
     {
       Spinor t[SPT];
       produce(F{}, 0, p);
+      RES_STAMP(1);
       __syncthreads();
       interior(F{}, p, t);
+      RES_STAMP(2);
       faces(F{}, 0, t);
+      RES_STAMP(3);
       dd = 0.0;
 #pragma unroll
       for (int k = 0; k < SPT; ++k) dd += spinor_norm2(t[k]);
       produce(T{}, 1, t);
       publish(dd, 0);
+      RES_STAMP(4);
       __syncthreads();
       interior(T{}, t, w);
+      RES_STAMP(5);
       faces(T{}, 1, w);
+      RES_STAMP(6);
     }
     const double den = total(0);
+    RES_STAMP(7);
     const double alpha = den > 0.0 ? rs / den : 0.0;
     const bool repl = (it % kResReplace) == 0;
     double rsn = 0.0;
@@ -295,7 +312,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
       publish(rsn, 1);
 #pragma unroll
       for (int k = 0; k < SPT; ++k) x[k] = sp_fma(alpha, p[k], x[k]);
+      RES_STAMP(8);
       rs_new = total(1);
+      RES_STAMP(9);
       check = rs_new <= t2lo;
       if (!check && rs_new <= t2hi) {
         double sq;
@@ -336,7 +355,9 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(LC * TC / (CS * BX 
     for (int k = 0; k < SPT; ++k) p[k] = sp_fma(beta, p[k], r[k]);
     rs = rs_new;
     inv_rs = __drcp_rn(rs);
+    RES_STAMP(10);
   }
+  RES_STAMP_END(a.maxiter);
 #pragma unroll
   for (int k = 0; k < SPT; ++k) st_spinor(a.x, cb + site(k), rot_out<ROT>(x[k]));
   if (tid == 0 && rank == 0) {
