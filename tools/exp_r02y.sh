@@ -1,4 +1,5 @@
 #!/bin/bash
+# Record of a round-2 experiment (the graph cache it measured was reverted: no gain).
 # Round-2: instantiated WHILE graphs of the decomposed CG kept per buffer set: DD tests, cfg5 line, trajectory breakdown
 set -u
 O=gpurun_out/exp_r02y
