@@ -388,7 +388,9 @@ struct WarpGen {
 // 0.5 s for cfg5's 25 M).  The words of a stream are random-access (Philox is
 // counter based); only the ziggurat's passes are serial, because a pass that
 // leaves the fast path consumes extra words.  The stream's words are cut into
-// chunks of kChunk:
+// chunks of C = kChunk words (SCH_NP_CHUNK sets another size: the tests walk
+// streams in chunks of a few words, where nearly every chunk is entered at an
+// offset and slow passes straddle several chunks):
 //   A  every warp walks its chunk as if a pass started at the chunk's first
 //      word: how many values the passes starting in the chunk return (cnt)
 //      and how many words the last one runs past the chunk's end (over);
@@ -421,7 +423,7 @@ struct OutMap {   // where value g of the stream goes
 struct ParArgs {
   NpPhilox* st;
   long long N;
-  int K;
+  int K, C;         // chunks, words per chunk
   int *cnt, *over, *entry;
   long long* pref;
   long long* tot;   // [0] values the chunks hold (capped at N), [1] first word after the chunks' passes
@@ -489,7 +491,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) k_np_par_count(ParArgs a)
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = blockIdx.x * kWarpsPerBlock + w;
   if (k >= a.K) return;
-  const long long start = a.st->pos + (long long)k * kChunk, end = start + kChunk;
+  const long long start = a.st->pos + (long long)k * a.C, end = start + a.C;
   WarpGen g;
   g.load_at(*a.st, rings[w], lane, start);
   const long long n = g.walk(end, 0, 0x7fffffffffffffffLL, [](long long, double) {});
@@ -516,7 +518,7 @@ __global__ void __launch_bounds__(32) k_np_par_scan(ParArgs a) {
       if (e != 0) {
         // passes from the assumed entry (word 0 of the chunk) and from the true
         // one (word e) until they stand on the same word
-        const long long s0 = a0 + (long long)(k0 + j) * kChunk, end = s0 + kChunk;
+        const long long s0 = a0 + (long long)(k0 + j) * a.C, end = s0 + a.C;
         long long pm = s0, pa = s0 + e;
         int cm = 0, ca = 0;
         while (pm != pa && (pm < end || pa < end)) {
@@ -558,7 +560,7 @@ __global__ void __launch_bounds__(32) k_np_par_scan(ParArgs a) {
   }
   if (lane == 0) {
     a.tot[0] = run < a.N ? run : a.N;
-    a.tot[1] = a0 + (long long)a.K * kChunk + e;
+    a.tot[1] = a0 + (long long)a.K * a.C + e;
   }
 }
 
@@ -569,7 +571,7 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) k_np_par_emit(ParArgs a) 
   if (k >= a.K) return;
   const long long g0 = a.pref[k];
   if (g0 >= a.N) return;   // warp-uniform
-  const long long start = a.st->pos + (long long)k * kChunk, end = start + kChunk;
+  const long long start = a.st->pos + (long long)k * a.C, end = start + a.C;
   WarpGen g;
   g.load_at(*a.st, rings[w], lane, start + a.entry[k]);
   const OutMap om = a.om;
@@ -682,8 +684,15 @@ int par_normals(sch_ctx* ctx, NpPhilox* st, long long N, const OutMap& om) {
   ParArgs a;
   a.st = st;
   a.N = N;
+  static int chunk = 0;
+  if (!chunk) {
+    const char* e = getenv("SCH_NP_CHUNK");
+    chunk = e ? atoi(e) : kChunk;
+    if (chunk < 1) chunk = kChunk;
+  }
+  a.C = chunk;
   const long long words = N + N / 50 + 4 * kChunk;   // 1.02 words per value (1.0127 expected)
-  a.K = (int)((words + kChunk - 1) / kChunk);
+  a.K = (int)((words + a.C - 1) / a.C);
   void* ws;
   const size_t ints = ((size_t)a.K * sizeof(int) + 255) & ~size_t(255);
   const size_t lls = ((size_t)a.K * sizeof(long long) + 255) & ~size_t(255);

@@ -225,17 +225,22 @@ np.savez(sys.argv[2], **out)
 def test_long_stream_parallel_walk_equals_serial_walk(tmp_path):
     """The whole-GPU walk of a long stream against the warp-per-stream walk
     (SCH_NP_PAR=0) on the same draws: values and the generator state left
-    behind, byte for byte.  The switch is read once per process."""
+    behind, byte for byte — with the production chunk of 2048 words and with
+    chunks of 7 and 33 words (SCH_NP_CHUNK), where most chunks are entered at
+    an offset, slow passes straddle chunk ends and a tail pass can swallow a
+    whole chunk.  The switches are read once per process."""
     import os
     import subprocess
     import sys
     from pathlib import Path
     root = str(Path(__file__).resolve().parent.parent)
     res = {}
-    for m in ("0", "1"):
-        path = tmp_path / f"par{m}.npz"
+    for name, env in (("serial", {"SCH_NP_PAR": "0"}), ("par", {}), ("par7", {"SCH_NP_CHUNK": "7"}),
+                      ("par33", {"SCH_NP_CHUNK": "33"})):
+        path = tmp_path / f"{name}.npz"
         subprocess.run([sys.executable, "-c", _PAR_SNIPPET, root, str(path)], check=True,
-                       env=dict(os.environ, SCH_NP_PAR=m), timeout=600)
-        res[m] = np.load(path)
-    for k in res["0"].files:
-        assert np.array_equal(res["0"][k], res["1"][k]), k
+                       env=dict(os.environ, **env), timeout=600)
+        res[name] = np.load(path)
+    for name in ("par", "par7", "par33"):
+        for k in res["serial"].files:
+            assert np.array_equal(res["serial"][k], res[name][k]), (name, k)
