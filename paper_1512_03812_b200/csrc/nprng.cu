@@ -17,6 +17,7 @@
 // The generator state lives in device memory between calls, so a chain's
 // stream advances exactly as the reference's Generator object would.
 #include "common.cuh"
+#include <algorithm>
 #include <cstdlib>
 
 #include "runtime.hpp"
@@ -587,6 +588,41 @@ __global__ void __launch_bounds__(32 * kWarpsPerBlock) k_np_par_emit(ParArgs a) 
   }
 }
 
+// uniforms of one long stream: one word each, so value i is word a0 + i —
+// a thread per Philox block; the last thread's block becomes the state
+__global__ void __launch_bounds__(256) k_np_par_doubles(NpPhilox* st, NpPhilox* st_end, double* __restrict__ out,
+                                                        long long n, int mode, double lo, double hi) {
+  const NpPhilox s = *st;
+  const long long a0 = s.pos, jl = (a0 + n - 1) / 4;
+  const double range = hi - lo;
+  for (long long j = a0 / 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; j <= jl;
+       j += (long long)gridDim.x * blockDim.x) {
+    uint64_t w[4];
+    uint64_t x0 = s.ctr[0] + (uint64_t)j, x1 = s.ctr[1], x2 = s.ctr[2], x3 = s.ctr[3];
+    if (x0 < s.ctr[0] && ++x1 == 0 && ++x2 == 0) ++x3;
+    if (j == 0) {
+      for (int e = 0; e < 4; ++e) w[e] = s.buf[e];
+    } else {
+      philox_block(x0, x1, x2, x3, s.key[0], s.key[1], w[0], w[1], w[2], w[3]);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const long long i = 4 * j + e - a0;
+      if (i < 0 || i >= n) continue;
+      const double u = (double)(w[e] >> 11) * (1.0 / 9007199254740992.0);
+      out[i] = mode == 1 ? __dadd_rn(lo, __dmul_rn(range, u)) : u;
+    }
+    if (j == jl) {   // NumPy's state after the last word
+      NpPhilox t = s;
+      t.ctr[0] = x0; t.ctr[1] = x1; t.ctr[2] = x2; t.ctr[3] = x3;
+      for (int e = 0; e < 4; ++e) t.buf[e] = w[e];
+      t.pos = (int)((a0 + n - 1) % 4) + 1;
+      *st_end = t;
+    }
+  }
+}
+__global__ void k_np_state_copy(NpPhilox* dst, const NpPhilox* src) { *dst = *src; }
+
 // the chunks held fewer than N values: the rest serially, from where they ended
 __global__ void __launch_bounds__(32) k_np_par_rest(ParArgs a) {
   __shared__ uint64_t ring[kRing];
@@ -740,6 +776,20 @@ int sch_np_rng_fill(sch_ctx* ctx, void* state, double* out, int B, long long n_p
       OutMap om{out + (long long)c * n_per_chain, nullptr, 0, 1.0, 0};
       const int rc = par_normals(ctx, (NpPhilox*)state + c, n_per_chain, om);
       if (rc) return rc;
+    }
+    return SCH_OK;
+  }
+  if (mode != 0 && par_stream(B, n_per_chain)) {   // the other warps of the launch read the old state
+    void* ws;
+    const int rc = sch_workspace(ctx, 256, &ws);
+    if (rc) return rc;
+    const unsigned grid = (unsigned)std::min<long long>((n_per_chain / 4 + 256) / 256, 148 * 8);
+    for (int c = 0; c < B; ++c) {
+      NpPhilox* sc = (NpPhilox*)state + c;
+      k_np_par_doubles<<<grid, 256, 0, ctx->stream>>>(sc, (NpPhilox*)ws, out + (long long)c * n_per_chain,
+                                                      n_per_chain, mode, lo, hi);
+      k_np_state_copy<<<1, 1, 0, ctx->stream>>>(sc, (const NpPhilox*)ws);
+      ctx->launches += 2;
     }
     return SCH_OK;
   }

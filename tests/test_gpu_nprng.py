@@ -180,6 +180,11 @@ def test_long_stream_parallel_walk_is_bit_identical():
     assert np.array_equal(got, r.standard_normal(n))
     assert np.array_equal(g.standard_normal((11,)).cpu().numpy()[0], r.standard_normal(11))
     assert g.random().cpu().numpy()[0] == r.random()
+    # uniforms of a long stream (a thread per Philox block), then normals again
+    assert np.array_equal(g.uniform(-np.pi, np.pi, (2, 300, 301)).cpu().numpy()[0],
+                          r.uniform(-np.pi, np.pi, size=(2, 300, 301)))
+    assert np.array_equal(g.uniform(0.0, 1.0, (131_073,)).cpu().numpy()[0], r.uniform(0.0, 1.0, size=131_073))
+    assert g.random().cpu().numpy()[0] == r.random()
     # a length just above the threshold of the parallel path, twice in a row
     for m in (131_072, 140_001):
         assert np.array_equal(g.standard_normal((m,)).cpu().numpy()[0], r.standard_normal(m)), m
@@ -212,6 +217,7 @@ sys.path.insert(0, sys.argv[1])
 import paper_1512_03812_b200 as sw
 g = sw.NumpyDeviceRng(seed=31, n_chains=3, stream0=9)
 out = {"u": g.uniform(0.0, 1.0, (2,)).cpu().numpy(),
+       "hs": g.hot_start(sw.LatticeGeom(300, 256)).cpu().numpy(),
        "a": g.standard_normal((700_001,)).cpu().numpy(),
        "b": g.standard_normal((150_000,)).cpu().numpy()}
 p, phi = g.heatbath(sw.LatticeGeom(192, 384))
