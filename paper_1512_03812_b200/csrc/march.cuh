@@ -3,8 +3,9 @@
 //
 // The tile kernels (tile.cuh; round 2's TMA-pipelined 2-D variant) stage a
 // 2-D region in shared memory and run D, then D^dag, as barrier-separated
-// phases of a CTA: at 2048^2 they reach 49-55 % of HBM, bound by those phases (ncu: barrier and
-// short-scoreboard stalls) and not by the memory system.  Here there is no
+// phases of a CTA: at 2048^2 they reach 49-55 % of HBM, bound by those
+// phases (ncu: barrier and short-scoreboard stalls) and not by the memory
+// system.  Here there is no
 // shared memory and no barrier: a WARP owns a band of kMarchW = 28 time
 // columns (lane l holds column c0 - 2 + l, i.e. the band plus the two halo
 // columns D^dag D needs on either side) and marches down the x rows of its
@@ -16,8 +17,8 @@
 // so every input value is loaded once per warp (coalesced 1-KiB spinor rows
 // and 512-B link rows), D v never leaves the register file and the output
 // row is stored as one 896-B run.  Loads run PF rows ahead of the arithmetic
-// in a register ring, which is what keeps HBM busy: a warp always has PF
-// rows (2-3 KiB) in flight and an SM holds 12-16 such warps.  The redundant
+// in a register ring, which is what keeps HBM busy: a warp always has PF = 4
+// rows (2-3 KiB each) in flight and an SM holds 8 such warps.  The redundant
 // work is the 4 halo lanes (12.5 %, L1/L2 hits: the 4 warps of a CTA own
 // adjacent bands) and the 4 pipeline-fill rows per segment.
 //
@@ -211,7 +212,9 @@ inline int march_nch(int T) { return T / kMarchCW; }
 // Measured on cfg5 (2048^2, profiles/r02/README.md): a 4-row register ring at
 // 2 CTAs/SM (8 warps per SM, ~96 KB of loads in flight per SM) is the best of
 // PF 1-6 x 2-4 CTAs/SM for all three modes; deeper rings spill, more warps
-// with shallower rings keep fewer bytes in flight.
+// with shallower rings keep fewer bytes in flight.  Shared-memory rings fed by
+// per-lane cp.async or by per-warp TMA bulk copies, and L2 prefetches ahead
+// of the ring, all measured slower.
 template <int MODE, int PF = 4, int MINB = 2>
 inline bool launch_dd_march(const TileArgs& t, cudaStream_t st, int num_sms) {
   MarchArgs a;
